@@ -1,0 +1,190 @@
+/*
+ * mpsg.h -- C ABI of the B200-native multi-precision sparse path.
+ *
+ * Drop-in boundary for the reference's hot path (paths under
+ * /root/reference/proj/include/mps/):
+ *
+ *   reference entry point (file:line)                       replaced by
+ *   ------------------------------------------------------  ----------------------
+ *   CsrMatrix<E> / CsrValues<MultiComponent<K>>             mpsg_csr_upload
+ *       (sparse.hpp:47-78; convert_csr sparse.hpp:195-207)
+ *   ComplexSparseMatrix<E> (sparse.hpp:221-230)             mpsg_csr_upload(is_complex=1)
+ *   spmv<E,F>(A, v, KernelMode) (kernels.hpp:348-366)       mpsg_spmv / mpsg_spmv_dev
+ *   spmv_complex<E,F>(A, v, KernelMode) (kernels.hpp:399)   mpsg_spmv_complex(_dev)
+ *   CsrOperator<E>::apply (krylov.hpp:101-120)              mpsg_spmv_dev (operator seam)
+ *   solve_cg<E,Op>(op, b, SolverConfig) (krylov.hpp:238)    mpsg_cg
+ *   detail::partition_rows (kernels.hpp:63-80)              mpsg_partition_rows
+ *   checksum (bench.hpp:113-150)                            mpsg_checksum(_complex)
+ *
+ * Conventions.
+ *  - K is the component count: 2 (double-double), 3 (triple-double),
+ *    4 (quad-double).
+ *  - Vectors are AoS: element i occupies doubles [i*K, i*K+K), which is the
+ *    memory image of std::vector<MultiComponent<K>> (MultiComponent<K> is a
+ *    std::array<double,K>, multicomp.hpp:17-30), so `v.data()` can be passed
+ *    as `const double*`.
+ *  - Matrix values are K component planes, planes[j][k] = component j of
+ *    nonzero k (CsrValues::component(j), sparse.hpp:63); complex matrices pass
+ *    2K planes (re components then im components) over one shared structure.
+ *  - Indices are int64 as in the reference (sparse.hpp:73-74); the device
+ *    keeps int32 and rejects anything that does not fit (MPSG_E_RANGE).
+ *  - order: MPSG_ORDER_SCALAR reproduces `lanes_enabled = false`
+ *    (row_sum_scalar, kernels.hpp:90-99) bit for bit; MPSG_ORDER_LANE4
+ *    reproduces the reference default `lanes_enabled = true`
+ *    (row_sum_lanes_pure, kernels.hpp:103-121) bit for bit; MPSG_ORDER_FAST
+ *    reorders long-row accumulation for throughput and is checked against the
+ *    componentwise bound |y - y_ref| <= 4 * rowlen * u * sum|a||x|.
+ *    KernelMode::threads has no device meaning and is ignored.
+ *  - Errors are returned as status codes; nothing crosses the ABI as an
+ *    exception.  mpsg_last_error(ctx) gives the message (for MPSG_E_DIM it is
+ *    the reference's std::invalid_argument text, kernels.hpp:333-339).
+ *  - A context is bound to one device and is not thread-safe (one host thread
+ *    per context).  Host-pointer calls are synchronous like the reference;
+ *    *_dev calls are stream-ordered and asynchronous.
+ */
+#ifndef MPSG_H
+#define MPSG_H
+
+#include <stdint.h>
+
+#if defined(_WIN32)
+#define MPSG_API
+#else
+#define MPSG_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPSG_VERSION_MAJOR 0
+#define MPSG_VERSION_MINOR 1
+
+enum mpsg_status {
+  MPSG_OK = 0,
+  MPSG_E_DIM = 1,    /* vector / matrix dimension mismatch (std::invalid_argument) */
+  MPSG_E_RANGE = 2,  /* index does not fit int32, or out of [0, ncols) */
+  MPSG_E_CUDA = 3,   /* CUDA runtime failure */
+  MPSG_E_NCCL = 4,   /* reserved for the multi-GPU layer */
+  MPSG_E_OOM = 5,    /* device allocation failed */
+  MPSG_E_ARG = 6,    /* invalid argument (K, order, null pointer, config) */
+  MPSG_E_STRUCT = 7  /* malformed CSR (indptr not monotone / wrong length) */
+};
+
+enum mpsg_order {
+  MPSG_ORDER_SCALAR = 0, /* lanes off: bit-exact with the reference */
+  MPSG_ORDER_LANE4 = 1,  /* lanes on (reference default): bit-exact */
+  MPSG_ORDER_FAST = 2    /* throughput order for long rows (bounded error) */
+};
+
+/* SolverStatus, krylov.hpp:46 */
+enum mpsg_solver_status {
+  MPSG_CONVERGED = 0,
+  MPSG_MAX_ITERATIONS = 1,
+  MPSG_BREAKDOWN = 2,
+  MPSG_DIVERGED = 3
+};
+
+typedef struct mpsg_ctx mpsg_ctx;
+typedef struct mpsg_csr mpsg_csr;
+
+/* Layout statistics of an uploaded matrix. */
+typedef struct mpsg_csr_stats {
+  int64_t nrows, ncols, nnz;
+  int32_t K, is_complex;
+  int64_t nslices;         /* SELL slices (short rows) */
+  int64_t sell_elems;      /* padded SELL elements */
+  int64_t nlong;           /* rows in the long-row store */
+  int64_t long_nnz;        /* nonzeros in the long-row store */
+  int64_t nchunks;         /* fast-mode warp chunks over long rows */
+  int64_t device_bytes;    /* device memory held by the matrix */
+} mpsg_csr_stats;
+
+/* SolverConfig subset used by CG (krylov.hpp:58-75). */
+typedef struct mpsg_cg_config {
+  double rel_tol;     /* default 1e-13 */
+  double abs_tol;     /* default 1e-99 */
+  int64_t max_iters;  /* default 10000 */
+  int32_t check_every; /* host polls the device status every N iterations (0 = 32) */
+  int32_t use_graph;   /* capture the iteration batch in a CUDA graph (default 1) */
+} mpsg_cg_config;
+
+/* SolverReport (krylov.hpp:77-88). */
+typedef struct mpsg_cg_report {
+  int32_t status; /* mpsg_solver_status */
+  int32_t converged;
+  int64_t iterations;
+  int64_t history_len; /* entries written to the caller's history buffer */
+  double rhs_norm;
+  double final_recurrence_residual;
+  double final_true_residual;
+  double setup_seconds;
+  double solve_seconds;
+  char detail[64];
+} mpsg_cg_report;
+
+/* ---- context --------------------------------------------------------- */
+MPSG_API int mpsg_ctx_create(int device, mpsg_ctx** out);
+MPSG_API void mpsg_ctx_destroy(mpsg_ctx* ctx);
+MPSG_API const char* mpsg_last_error(const mpsg_ctx* ctx);
+/* Use a caller-owned cudaStream_t (as void*) for subsequent work; NULL
+ * restores the context's own stream. */
+MPSG_API int mpsg_ctx_set_stream(mpsg_ctx* ctx, void* stream);
+/* Tunables (0 keeps the default): long-row threshold (256), SELL sort window
+ * (16384 rows), fast-mode chunk length (2048). Affect later uploads. */
+MPSG_API int mpsg_ctx_set_layout(mpsg_ctx* ctx, int64_t long_threshold, int64_t sigma, int64_t fast_chunk);
+/* Block until all work queued on the context's stream has finished. */
+MPSG_API int mpsg_ctx_synchronize(mpsg_ctx* ctx);
+
+/* ---- matrices -------------------------------------------------------- */
+/* Copies a host CSR (reference layout) to the device once.  planes has K
+ * (real) or 2K (complex) entries, each nnz = indptr[nrows] doubles. */
+MPSG_API int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t ncols,
+                    const int64_t* indptr, const int64_t* indices, const double* const* planes,
+                    mpsg_csr** out);
+MPSG_API void mpsg_csr_destroy(mpsg_csr* A);
+MPSG_API int mpsg_csr_get_stats(const mpsg_csr* A, mpsg_csr_stats* out);
+
+/* ---- SpMV (kernels.hpp:348-366, 399-416) ------------------------------ */
+/* Host pointers, synchronous: y[nrows*K] = A x[xlen*K]. */
+MPSG_API int mpsg_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen, const double* x,
+              double* y);
+/* Device pointers, asynchronous on `stream` (NULL: the context stream). */
+MPSG_API int mpsg_spmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_x, double* d_y,
+                  void* stream);
+MPSG_API int mpsg_spmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen,
+                      const double* x_re, const double* x_im, double* y_re, double* y_im);
+MPSG_API int mpsg_spmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_x_re,
+                          const double* d_x_im, double* d_y_re, double* d_y_im, void* stream);
+
+/* ---- conjugate gradient (krylov.hpp:238-281) -------------------------- */
+/* Device-resident CG on A (real, square).  b and x0 (NULL = zero start) are
+ * host AoS vectors of length nrows; x_out receives the iterate; history
+ * receives ||r_k|| for k = 0.. (up to history_cap entries). */
+MPSG_API int mpsg_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, const double* b,
+            const double* x0, const mpsg_cg_config* cfg, double* x_out, double* history,
+            int64_t history_cap, mpsg_cg_report* report);
+
+/* ---- host utilities ---------------------------------------------------- */
+/* nnz-balanced contiguous row bounds (kernels.hpp:63-80), parts+1 entries. */
+MPSG_API int mpsg_partition_rows(const int64_t* indptr, int64_t nrows, int parts, int64_t* bounds);
+/* FNV-1a over component bits in AoS order (bench.hpp:113-150). */
+MPSG_API uint64_t mpsg_checksum(int K, int64_t n, const double* v);
+MPSG_API uint64_t mpsg_checksum_complex(int K, int64_t n, const double* re, const double* im);
+MPSG_API const char* mpsg_version(void);
+
+/* ---- measurement / verification -------------------------------------- */
+/* fp64-pipe throughput (DFMA instructions per second) on the context device:
+ * the roofline denominator for the fp64-bound TD/QD configurations. */
+MPSG_API int mpsg_measure_fp64_peak(mpsg_ctx* ctx, double* ops_per_s);
+/* Batched device multi-component op on AoS device arrays (n elements of K):
+ * op 0 add, 1 mul, 2 mul_by_double(a, b[i][0]), 3 sub, 4 divide, 5 sqrt(a)
+ * (multicomp.hpp:225-322).  Asynchronous on the context stream. */
+MPSG_API int mpsg_mc_op_dev(mpsg_ctx* ctx, int op, int K, int64_t n, const double* d_a,
+                            const double* d_b, double* d_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPSG_H */

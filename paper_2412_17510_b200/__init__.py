@@ -1,0 +1,424 @@
+"""B200-native multi-precision CSR SpMV (DD/TD/QD, real and complex) and CG.
+
+Host-side mirror of the reference's interface for this path, calling the
+CUDA library ``libmpsg.so`` through its C ABI (include/mpsg.h).  Names,
+argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/mps/):
+
+  reference                                   here
+  ------------------------------------------  ------------------------------------
+  CsrMatrix<E> (sparse.hpp:69-78)              DeviceCsr (uploaded once)
+  KernelMode (kernels.hpp:39-45)               KernelMode (threads ignored; lanes
+                                               selects LANE4 / SCALAR; fast=True
+                                               selects the throughput order)
+  spmv(A, v, mode) (kernels.hpp:348)           spmv(A, v, mode)
+  spmv_complex(A, v, mode) (kernels.hpp:399)   spmv_complex(A, v_re, v_im, mode)
+  CsrOperator (krylov.hpp:101-120)             CsrOperator
+  SolverConfig / SolverReport (krylov.hpp)     SolverConfig / SolverReport
+  solve_cg(op, b, cfg) (krylov.hpp:238)        solve_cg(op, b, cfg)
+  partition_rows (kernels.hpp:63-80)           partition_rows
+  checksum (bench.hpp:113-150)                 checksum / checksum_complex
+
+Vectors are numpy float64 arrays of shape (n, K): the memory image of
+``std::vector<MultiComponent<K>>``.  ``std::invalid_argument`` becomes
+``ValueError`` with the reference's message text.  There is no CPU
+fallback: if the CUDA library or a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpsg.so")
+
+ORDER_SCALAR, ORDER_LANE4, ORDER_FAST = 0, 1, 2
+E_OK, E_DIM, E_RANGE, E_CUDA, E_NCCL, E_OOM, E_ARG, E_STRUCT = range(8)
+
+_P = ctypes.c_void_p
+_i64, _i32, _f64, _u64 = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_uint64
+
+
+class MpsgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[mpsg error {code}] {msg}")
+        self.code = code
+
+
+class CsrStats(ctypes.Structure):
+    _fields_ = [("nrows", _i64), ("ncols", _i64), ("nnz", _i64), ("K", ctypes.c_int32),
+                ("is_complex", ctypes.c_int32), ("nslices", _i64), ("sell_elems", _i64),
+                ("nlong", _i64), ("long_nnz", _i64), ("nchunks", _i64), ("device_bytes", _i64)]
+
+
+class _CgConfig(ctypes.Structure):
+    _fields_ = [("rel_tol", _f64), ("abs_tol", _f64), ("max_iters", _i64),
+                ("check_every", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+
+
+class _CgReport(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("converged", ctypes.c_int32), ("iterations", _i64),
+                ("history_len", _i64), ("rhs_norm", _f64), ("final_recurrence_residual", _f64),
+                ("final_true_residual", _f64), ("setup_seconds", _f64), ("solve_seconds", _f64),
+                ("detail", ctypes.c_char * 64)]
+
+
+_lib = None
+
+# every symbol include/mpsg.h declares
+EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_set_stream",
+           "mpsg_ctx_set_layout", "mpsg_ctx_synchronize", "mpsg_csr_upload", "mpsg_csr_destroy",
+           "mpsg_csr_get_stats", "mpsg_spmv", "mpsg_spmv_dev", "mpsg_spmv_complex",
+           "mpsg_spmv_complex_dev", "mpsg_cg", "mpsg_partition_rows", "mpsg_checksum",
+           "mpsg_checksum_complex", "mpsg_version", "mpsg_measure_fp64_peak", "mpsg_mc_op_dev")
+
+
+def lib():
+    """Load libmpsg.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                          "(make -C paper_2412_17510_b200/csrc)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.mpsg_ctx_create.argtypes = [_i32, ctypes.POINTER(_P)]
+    L.mpsg_ctx_destroy.argtypes = [_P]
+    L.mpsg_last_error.argtypes = [_P]
+    L.mpsg_last_error.restype = ctypes.c_char_p
+    L.mpsg_ctx_set_stream.argtypes = [_P, _P]
+    L.mpsg_ctx_set_layout.argtypes = [_P, _i64, _i64, _i64]
+    L.mpsg_ctx_synchronize.argtypes = [_P]
+    L.mpsg_csr_upload.argtypes = [_P, _i32, _i32, _i64, _i64, _P, _P, ctypes.POINTER(_P),
+                                  ctypes.POINTER(_P)]
+    L.mpsg_csr_destroy.argtypes = [_P]
+    L.mpsg_csr_get_stats.argtypes = [_P, ctypes.POINTER(CsrStats)]
+    L.mpsg_spmv.argtypes = [_P, _P, _i32, _i64, _P, _P]
+    L.mpsg_spmv_dev.argtypes = [_P, _P, _i32, _P, _P, _P]
+    L.mpsg_spmv_complex.argtypes = [_P, _P, _i32, _i64, _P, _P, _P, _P]
+    L.mpsg_spmv_complex_dev.argtypes = [_P, _P, _i32, _P, _P, _P, _P, _P]
+    L.mpsg_cg.argtypes = [_P, _P, _i32, _i64, _P, _P, ctypes.POINTER(_CgConfig), _P, _P, _i64,
+                          ctypes.POINTER(_CgReport)]
+    L.mpsg_partition_rows.argtypes = [_P, _i64, _i32, _P]
+    L.mpsg_checksum.argtypes = [_i32, _i64, _P]
+    L.mpsg_checksum.restype = _u64
+    L.mpsg_checksum_complex.argtypes = [_i32, _i64, _P, _P]
+    L.mpsg_checksum_complex.restype = _u64
+    L.mpsg_version.restype = ctypes.c_char_p
+    L.mpsg_measure_fp64_peak.argtypes = [_P, ctypes.POINTER(_f64)]
+    L.mpsg_mc_op_dev.argtypes = [_P, _i32, _i32, _i64, _P, _P, _P]
+    _lib = L
+    return L
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def _aos(v, name="vector") -> np.ndarray:
+    a = np.ascontiguousarray(v, dtype=np.float64)
+    if a.ndim != 2 or a.shape[1] not in (2, 3, 4):
+        raise ValueError(f"{name}: expected an (n, K) float64 array with K in 2..4, got {a.shape}")
+    return a
+
+
+# --------------------------------------------------------------------------- context
+class Context:
+    """One device, one stream (mpsg_ctx).  Not thread-safe, like the C ABI."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = _P()
+        rc = lib().mpsg_ctx_create(device, ctypes.byref(h))
+        if rc != E_OK:
+            raise MpsgError(rc, f"mpsg_ctx_create(device={device}) failed (no usable GPU?)")
+        self.h = h
+
+    def check(self, rc: int):
+        if rc == E_OK:
+            return
+        msg = lib().mpsg_last_error(self.h).decode()
+        if rc == E_DIM:
+            raise ValueError(msg)
+        raise MpsgError(rc, msg)
+
+    def set_stream(self, stream_ptr: int | None):
+        self.check(lib().mpsg_ctx_set_stream(self.h, stream_ptr))
+
+    def set_layout(self, long_threshold=0, sigma=0, fast_chunk=0):
+        self.check(lib().mpsg_ctx_set_layout(self.h, long_threshold, sigma, fast_chunk))
+
+    def synchronize(self):
+        self.check(lib().mpsg_ctx_synchronize(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mpsg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("MPSG_DEVICE", "0")))
+    return _default_ctx
+
+
+# --------------------------------------------------------------------------- matrices
+class DeviceCsr:
+    """Device copy of a reference CSR (``CsrMatrix<MultiComponent<K>>`` or a
+    ``ComplexSparseMatrix`` sharing one structure).
+
+    ``A`` is any object with ``nrows, ncols, indptr (int64), indices (int64),
+    planes`` ([K, nnz] real, [2K, nnz] complex).
+    """
+
+    def __init__(self, A, K: int, is_complex: bool = False, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.K = K
+        self.is_complex = bool(is_complex)
+        self.nrows, self.ncols = int(A.nrows), int(A.ncols)
+        indptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(A.indices, dtype=np.int64)
+        nplanes = 2 * K if is_complex else K
+        planes = np.asarray(A.planes)
+        if planes.shape[0] < nplanes:
+            raise ValueError(f"DeviceCsr: need {nplanes} value planes, got {planes.shape[0]}")
+        plist = [np.ascontiguousarray(planes[j], dtype=np.float64) for j in range(nplanes)]
+        parr = (_P * nplanes)(*[p.ctypes.data for p in plist])
+        h = _P()
+        self.ctx.check(lib().mpsg_csr_upload(self.ctx.h, K, 1 if is_complex else 0, self.nrows, self.ncols,
+                                             _p(indptr), _p(indices), parr, ctypes.byref(h)))
+        self.h = h
+        self.nnz = int(indptr[-1])
+
+    def stats(self) -> CsrStats:
+        s = CsrStats()
+        self.ctx.check(lib().mpsg_csr_get_stats(self.h, ctypes.byref(s)))
+        return s
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mpsg_csr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class KernelMode:
+    """kernels.hpp:39-45.  ``threads`` has no device meaning; ``lanes_enabled``
+    picks the bit-exact order; ``fast`` picks the throughput order."""
+
+    threads: int = 1
+    lanes_enabled: bool = True
+    fast: bool = False
+
+    @property
+    def order(self) -> int:
+        if self.fast:
+            return ORDER_FAST
+        return ORDER_LANE4 if self.lanes_enabled else ORDER_SCALAR
+
+
+def _order(mode) -> int:
+    if mode is None:
+        return ORDER_LANE4
+    if isinstance(mode, int):
+        return mode
+    return mode.order
+
+
+def spmv(A: DeviceCsr, v, mode: KernelMode | int | None = None) -> np.ndarray:
+    """y = A v (kernels.hpp:348-366); host arrays in, host array out."""
+    x = _aos(v, "spmv")
+    if x.shape[1] != A.K:
+        raise ValueError(f"spmv: vector has K={x.shape[1]} components, matrix has K={A.K}")
+    y = np.empty((A.nrows, A.K))
+    A.ctx.check(lib().mpsg_spmv(A.ctx.h, A.h, _order(mode), x.shape[0], _p(x), _p(y)))
+    return y
+
+
+def spmv_complex(A: DeviceCsr, v_re, v_im, mode: KernelMode | int | None = None):
+    """(y_re, y_im) = A v (kernels.hpp:399-416)."""
+    xr, xi = _aos(v_re, "spmv_complex"), _aos(v_im, "spmv_complex")
+    if xr.shape[0] != xi.shape[0]:
+        raise ValueError("spmv_complex: re/im vector length mismatch")
+    yr, yi = np.empty((A.nrows, A.K)), np.empty((A.nrows, A.K))
+    A.ctx.check(lib().mpsg_spmv_complex(A.ctx.h, A.h, _order(mode), xr.shape[0], _p(xr), _p(xi), _p(yr),
+                                        _p(yi)))
+    return yr, yi
+
+
+def spmv_dev(A: DeviceCsr, d_x: int, d_y: int, order: int = ORDER_LANE4, stream: int | None = None):
+    """Device-pointer SpMV, asynchronous on ``stream`` (a cudaStream_t as int)."""
+    A.ctx.check(lib().mpsg_spmv_dev(A.ctx.h, A.h, order, d_x, d_y, stream))
+
+
+def spmv_complex_dev(A: DeviceCsr, d_xr: int, d_xi: int, d_yr: int, d_yi: int, order: int = ORDER_LANE4,
+                     stream: int | None = None):
+    A.ctx.check(lib().mpsg_spmv_complex_dev(A.ctx.h, A.h, order, d_xr, d_xi, d_yr, d_yi, stream))
+
+
+# --------------------------------------------------------------------------- solver
+class SolverStatus(enum.IntEnum):  # krylov.hpp:46
+    Converged = 0
+    MaxIterations = 1
+    Breakdown = 2
+    Diverged = 3
+
+
+@dataclass
+class SolverConfig:  # krylov.hpp:58-75 (CG subset)
+    rel_tol: float = 1e-13
+    abs_tol: float = 1e-99
+    max_iters: int = 10000
+    threads: int = 1
+    lanes_enabled: bool = True
+    fast: bool = False
+    x0: Sequence[float] | None = None
+    check_every: int = 32
+    use_graph: bool = True
+
+    def validate(self):
+        if not (self.rel_tol > 0.0) or not (self.abs_tol > 0.0):
+            raise ValueError("solver: tolerances must be positive")
+        if self.max_iters < 1:
+            raise ValueError("solver: max_iters must be at least 1")
+        if self.threads < 1:
+            raise ValueError("solver: threads must be at least 1")
+
+
+@dataclass
+class SolverReport:  # krylov.hpp:77-88
+    status: SolverStatus = SolverStatus.MaxIterations
+    converged: bool = False
+    detail: str = ""
+    iterations: int = 0
+    residual_history: list = field(default_factory=list)
+    rhs_norm: float = 0.0
+    final_recurrence_residual: float = 0.0
+    final_true_residual: float = 0.0
+    setup_seconds: float = 0.0
+    solve_seconds: float = 0.0
+
+
+@dataclass
+class SolveResult:  # krylov.hpp:90-94
+    x: np.ndarray
+    report: SolverReport
+
+
+@dataclass
+class CsrOperator:
+    """krylov.hpp:101-120: the matrix side of a solve."""
+
+    matrix: DeviceCsr
+    threads: int = 1
+    lanes_enabled: bool = True
+    fast: bool = False
+
+    def rows(self) -> int:
+        return self.matrix.nrows
+
+    def cols(self) -> int:
+        return self.matrix.ncols
+
+    def mode(self) -> KernelMode:
+        return KernelMode(self.threads, self.lanes_enabled, self.fast)
+
+    def apply(self, x):
+        return spmv(self.matrix, x, self.mode())
+
+
+def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:
+    """Device-resident CG (krylov.hpp:238-281)."""
+    cfg = cfg or SolverConfig()
+    cfg.validate()
+    A = op.matrix
+    bb = _aos(b, "solver")
+    if op.rows() != op.cols():
+        raise ValueError(f"solver: operator must be square, got {op.rows()}x{op.cols()}")
+    if bb.shape[0] != op.cols():
+        raise ValueError("solver: rhs length does not match the operator")
+    x0 = None
+    if cfg.x0 is not None and len(cfg.x0) > 0:
+        if len(cfg.x0) != bb.shape[0]:
+            raise ValueError("solver: x0 length does not match the rhs")
+        x0 = np.zeros_like(bb)
+        x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)  # scalar_like (krylov.hpp:178)
+    c = _CgConfig(cfg.rel_tol, cfg.abs_tol, cfg.max_iters, cfg.check_every, 1 if cfg.use_graph else 0)
+    rep = _CgReport()
+    x = np.empty_like(bb)
+    hist = np.empty(cfg.max_iters + 1)
+    order = ORDER_FAST if (cfg.fast or op.fast) else (ORDER_LANE4 if (cfg.lanes_enabled and op.lanes_enabled)
+                                                       else ORDER_SCALAR)
+    A.ctx.check(lib().mpsg_cg(A.ctx.h, A.h, order, bb.shape[0], _p(bb), _p(x0), ctypes.byref(c), _p(x),
+                              _p(hist), len(hist), ctypes.byref(rep)))
+    report = SolverReport(
+        status=SolverStatus(rep.status), converged=bool(rep.converged), detail=rep.detail.decode(),
+        iterations=int(rep.iterations), residual_history=hist[: rep.history_len].tolist(),
+        rhs_norm=rep.rhs_norm, final_recurrence_residual=rep.final_recurrence_residual,
+        final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
+        solve_seconds=rep.solve_seconds)
+    return SolveResult(x, report)
+
+
+# --------------------------------------------------------------------------- host utilities
+def partition_rows(indptr, nrows: int, parts: int) -> np.ndarray:
+    """nnz-balanced contiguous row bounds (kernels.hpp:63-80)."""
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    out = np.empty(parts + 1, dtype=np.int64)
+    rc = lib().mpsg_partition_rows(_p(ip), nrows, parts, _p(out))
+    if rc != E_OK:
+        raise ValueError("partition_rows: bad arguments")
+    return out
+
+
+def checksum(v) -> int:
+    a = _aos(v, "checksum")
+    return int(lib().mpsg_checksum(a.shape[1], a.shape[0], _p(a)))
+
+
+def checksum_complex(re, im) -> int:
+    r, i = _aos(re), _aos(im)
+    return int(lib().mpsg_checksum_complex(r.shape[1], r.shape[0], _p(r), _p(i)))
+
+
+def measure_fp64_peak(ctx: Optional[Context] = None) -> float:
+    """fp64 instructions per second (DFMA throughput) on the context's GPU."""
+    ctx = ctx or default_context()
+    v = _f64()
+    ctx.check(lib().mpsg_measure_fp64_peak(ctx.h, ctypes.byref(v)))
+    return float(v.value)
+
+
+MC_OPS = {"add": 0, "mul": 1, "mul_d": 2, "sub": 3, "div": 4, "sqrt": 5}
+
+
+def mc_op_dev(ctx: Context, op: str, K: int, n: int, d_a: int, d_b: int, d_out: int):
+    """Batched device MC op on AoS device arrays (asynchronous on the context stream)."""
+    ctx.check(lib().mpsg_mc_op_dev(ctx.h, MC_OPS[op], K, n, d_a, d_b, d_out))
+
+
+def version() -> str:
+    return lib().mpsg_version().decode()

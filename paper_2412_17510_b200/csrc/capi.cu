@@ -1,0 +1,505 @@
+// capi.cu -- host side of the C ABI declared in include/mpsg.h.
+//
+// Owns device memory, streams and the one-time re-layout of a reference CSR
+// (int64 indptr/indices + K SoA planes, sparse.hpp:47-78) into the device
+// layout described in layout.h, and dispatches the SpMV / CG launchers that
+// live in the per-K translation units.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace mpsg;
+
+namespace {
+
+template <class T>
+int dev_alloc(mpsg_ctx* ctx, mpsg_csr* A, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+  A->device_bytes += (int64_t)(count * sizeof(T));
+  return MPSG_OK;
+}
+
+int ensure_scratch(mpsg_ctx* ctx, int slot, size_t bytes) {
+  if (ctx->dcap[slot] >= bytes) return MPSG_OK;
+  if (ctx->dbuf[slot]) cudaFree(ctx->dbuf[slot]);
+  ctx->dbuf[slot] = nullptr;
+  ctx->dcap[slot] = 0;
+  CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->dbuf[slot]), bytes ? bytes : 8));
+  ctx->dcap[slot] = bytes;
+  return MPSG_OK;
+}
+
+// ---- upload helper kernels --------------------------------------------
+// SELL build: thread per slot, k loop; padding gets col 0 / value 0.
+__global__ void build_sell_kernel(int64_t nslots, int C, const int64_t* slice_ptr,
+                                  const int* slot_row, const int* slot_len, const int64_t* indptr,
+                                  const int64_t* indices, const double* planes, int nplanes,
+                                  int64_t nnz, int64_t ncols, int* scol, double* sval,
+                                  int64_t stride, int* bad) {
+  int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (slot >= nslots) return;
+  const int64_t s = slot / C, t = slot % C;
+  const int64_t base = slice_ptr[s] + t;
+  const int slen = (int)((slice_ptr[s + 1] - slice_ptr[s]) / C);
+  const int row = slot_row[slot], len = slot_len[slot];
+  const int64_t src0 = row >= 0 ? indptr[row] : 0;
+  for (int k = 0; k < slen; ++k) {
+    const int64_t dst = base + (int64_t)k * C;
+    if (k < len) {
+      const int64_t c = indices[src0 + k];
+      if (c < 0 || c >= ncols) *bad = 1;
+      scol[dst] = (int)c;
+      for (int j = 0; j < nplanes; ++j) sval[j * stride + dst] = planes[j * nnz + src0 + k];
+    } else {
+      scol[dst] = 0;
+      for (int j = 0; j < nplanes; ++j) sval[j * stride + dst] = 0.0;
+    }
+  }
+}
+
+// Long store build: one block per long row, contiguous copy.
+__global__ void build_long_kernel(const int* lrow, const int64_t* lptr, const int64_t* indptr,
+                                  const int64_t* indices, const double* planes, int nplanes,
+                                  int64_t nnz, int64_t ncols, int* lcol, double* lval,
+                                  int64_t stride, int* bad) {
+  const int r = blockIdx.x;
+  const int64_t src0 = indptr[lrow[r]];
+  const int64_t dst0 = lptr[r], len = lptr[r + 1] - dst0;
+  for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
+    const int64_t c = indices[src0 + k];
+    if (c < 0 || c >= ncols) *bad = 1;
+    lcol[dst0 + k] = (int)c;
+    for (int j = 0; j < nplanes; ++j) lval[j * stride + dst0 + k] = planes[j * nnz + src0 + k];
+  }
+}
+
+void free_csr(mpsg_csr* A) {
+  if (!A) return;
+  void* ptrs[] = {A->slice_ptr, A->slot_row, A->slot_len, A->scol,  A->sval,
+                  A->lrow,      A->lptr,     A->lcol,     A->lval,  A->chunk_row,
+                  A->chunk_first, A->partial, A->counter};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete A;
+}
+
+std::string dim_msg(const char* what, int64_t vsize, int64_t ncols) {
+  // kernels.hpp:333-339
+  return std::string(what) + ": vector length " + std::to_string(vsize) +
+         " does not match matrix dimension " + std::to_string(ncols);
+}
+
+
+}  // namespace
+
+namespace mpsg {
+int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
+                double* yre, double* yim, cudaStream_t st) {
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "spmv: unknown order %d", order);
+  if (A->nrows == 0) return MPSG_OK;
+  if (!A->cplx) {
+    switch (A->K) {
+      case 2: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st);
+      case 3: return launch_spmv_k<3, false>(ctx, A, order, xre, xim, yre, yim, st);
+      case 4: return launch_spmv_k<4, false>(ctx, A, order, xre, xim, yre, yim, st);
+    }
+  } else {
+    switch (A->K) {
+      case 2: return launch_spmv_k<2, true>(ctx, A, order, xre, xim, yre, yim, st);
+      case 3: return launch_spmv_k<3, true>(ctx, A, order, xre, xim, yre, yim, st);
+      case 4: return launch_spmv_k<4, true>(ctx, A, order, xre, xim, yre, yim, st);
+    }
+  }
+  return fail(ctx, MPSG_E_ARG, "spmv: unsupported K %d", A->K);
+}
+
+}  // namespace mpsg
+
+// ==========================================================================
+extern "C" {
+
+const char* mpsg_version(void) { return "mpsg 0.1 (sm_100a)"; }
+
+int mpsg_ctx_create(int device, mpsg_ctx** out) {
+  if (!out) return MPSG_E_ARG;
+  *out = nullptr;
+  auto* ctx = new mpsg_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return MPSG_E_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  if (const char* s = std::getenv("MPSG_LONG_THRESHOLD")) ctx->long_threshold = std::atoll(s);
+  if (const char* s = std::getenv("MPSG_SIGMA")) ctx->sigma = std::atoll(s);
+  if (const char* s = std::getenv("MPSG_FAST_CHUNK")) ctx->fast_chunk = std::atoll(s);
+  *out = ctx;
+  return MPSG_OK;
+}
+
+void mpsg_ctx_destroy(mpsg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (auto& p : ctx->dbuf)
+    if (p) cudaFree(p);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* mpsg_last_error(const mpsg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int mpsg_ctx_set_stream(mpsg_ctx* ctx, void* stream) {
+  if (!ctx) return MPSG_E_ARG;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return MPSG_OK;
+}
+
+int mpsg_ctx_set_layout(mpsg_ctx* ctx, int64_t long_threshold, int64_t sigma, int64_t fast_chunk) {
+  if (!ctx) return MPSG_E_ARG;
+  if (long_threshold > 0) ctx->long_threshold = long_threshold;
+  if (sigma > 0) ctx->sigma = sigma;
+  if (fast_chunk > 0) {
+    if (fast_chunk % 32) return fail(ctx, MPSG_E_ARG, "fast_chunk must be a multiple of 32");
+    ctx->fast_chunk = fast_chunk;
+  }
+  return MPSG_OK;
+}
+
+int mpsg_ctx_synchronize(mpsg_ctx* ctx) {
+  if (!ctx) return MPSG_E_ARG;
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return MPSG_OK;
+}
+
+int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t ncols,
+                    const int64_t* indptr, const int64_t* indices, const double* const* planes,
+                    mpsg_csr** out) {
+  if (!ctx || !out) return MPSG_E_ARG;
+  *out = nullptr;
+  if (K < 2 || K > 4) return fail(ctx, MPSG_E_ARG, "csr_upload: K must be 2, 3 or 4 (got %d)", K);
+  if (nrows < 0 || ncols < 0 || !indptr) return fail(ctx, MPSG_E_ARG, "csr_upload: bad shape");
+  const int64_t I32 = std::numeric_limits<int>::max();
+  if (nrows > I32 || ncols > I32)
+    return fail(ctx, MPSG_E_RANGE, "csr_upload: %lld x %lld exceeds the int32 index range",
+                (long long)nrows, (long long)ncols);
+  if (indptr[0] != 0) return fail(ctx, MPSG_E_STRUCT, "csr_upload: indptr[0] must be 0");
+  const int64_t nnz = indptr[nrows];
+  const int nplanes = is_complex ? 2 * K : K;
+  if (nnz > 0 && (!indices || !planes)) return fail(ctx, MPSG_E_ARG, "csr_upload: null arrays");
+  for (int j = 0; j < nplanes && nnz > 0; ++j)
+    if (!planes[j]) return fail(ctx, MPSG_E_ARG, "csr_upload: null plane %d", j);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+
+  auto* A = new mpsg_csr();
+  std::unique_ptr<mpsg_csr, void (*)(mpsg_csr*)> holder(A, free_csr);
+  A->K = K;
+  A->cplx = is_complex != 0;
+  A->nrows = nrows;
+  A->ncols = ncols;
+  A->nnz = nnz;
+  A->C = A->cplx ? 16 : 32;
+  A->chunk = ctx->fast_chunk;
+  const int C = A->C;
+  const int64_t T = ctx->long_threshold;
+
+  // ---- host planning: row classes, windowed length sort, slices
+  std::vector<int> short_rows;
+  std::vector<int> long_rows;
+  short_rows.reserve((size_t)nrows);
+  for (int64_t i = 0; i < nrows; ++i) {
+    const int64_t len = indptr[i + 1] - indptr[i];
+    if (len < 0) return fail(ctx, MPSG_E_STRUCT, "csr_upload: indptr not monotone at row %lld", (long long)i);
+    if (len > T)
+      long_rows.push_back((int)i);
+    else
+      short_rows.push_back((int)i);
+  }
+  // stable counting sort by length, descending, inside windows of sigma rows
+  {
+    std::vector<int> sorted(short_rows.size());
+    std::vector<int64_t> cnt((size_t)T + 2);
+    const size_t W = (size_t)std::max<int64_t>(1, ctx->sigma);
+    for (size_t w0 = 0; w0 < short_rows.size(); w0 += W) {
+      const size_t w1 = std::min(short_rows.size(), w0 + W);
+      std::fill(cnt.begin(), cnt.end(), 0);
+      for (size_t i = w0; i < w1; ++i) {
+        const int64_t len = indptr[short_rows[i] + 1] - indptr[short_rows[i]];
+        cnt[(size_t)(T - len)]++;
+      }
+      int64_t acc = (int64_t)w0;
+      for (auto& c : cnt) {
+        const int64_t v = c;
+        c = acc;
+        acc += v;
+      }
+      for (size_t i = w0; i < w1; ++i) {
+        const int64_t len = indptr[short_rows[i] + 1] - indptr[short_rows[i]];
+        sorted[(size_t)cnt[(size_t)(T - len)]++] = short_rows[i];
+      }
+    }
+    short_rows.swap(sorted);
+  }
+  A->nslices = ((int64_t)short_rows.size() + C - 1) / C;
+  std::vector<int> slot_row((size_t)(A->nslices * C), -1), slot_len((size_t)(A->nslices * C), 0);
+  std::vector<int64_t> slice_ptr((size_t)A->nslices + 1, 0);
+  for (int64_t s = 0; s < A->nslices; ++s) {
+    int mx = 0;
+    for (int t = 0; t < C; ++t) {
+      const int64_t i = s * C + t;
+      if (i < (int64_t)short_rows.size()) {
+        const int row = short_rows[(size_t)i];
+        const int len = (int)(indptr[row + 1] - indptr[row]);
+        slot_row[(size_t)i] = row;
+        slot_len[(size_t)i] = len;
+        mx = std::max(mx, len);
+      }
+    }
+    slice_ptr[(size_t)s + 1] = slice_ptr[(size_t)s] + (int64_t)mx * C;
+  }
+  A->sell_elems = slice_ptr.back();
+  // long store plan
+  A->nlong = (int64_t)long_rows.size();
+  std::vector<int64_t> lptr((size_t)A->nlong + 1, 0);
+  std::vector<int> chunk_first((size_t)A->nlong + 1, 0), chunk_row;
+  for (int64_t r = 0; r < A->nlong; ++r) {
+    const int row = long_rows[(size_t)r];
+    const int64_t len = indptr[row + 1] - indptr[row];
+    lptr[(size_t)r + 1] = lptr[(size_t)r] + len;
+    const int64_t nch = (len + A->chunk - 1) / A->chunk;
+    chunk_first[(size_t)r + 1] = chunk_first[(size_t)r] + (int)nch;
+    for (int64_t c = 0; c < nch; ++c) chunk_row.push_back((int)r);
+  }
+  A->long_nnz = lptr.back();
+  A->nchunks = (int64_t)chunk_row.size();
+
+  // ---- device staging of the reference arrays
+  int64_t* d_indptr = nullptr;
+  int64_t* d_indices = nullptr;
+  double* d_planes = nullptr;
+  int* d_bad = nullptr;
+  auto free_stage = [&]() {
+    if (d_indptr) cudaFree(d_indptr);
+    if (d_indices) cudaFree(d_indices);
+    if (d_planes) cudaFree(d_planes);
+    if (d_bad) cudaFree(d_bad);
+  };
+  struct StageGuard {
+    std::function<void()> f;
+    ~StageGuard() { f(); }
+  };
+  StageGuard sg{free_stage};
+  CUDA_TRY(ctx, cudaMalloc(&d_indptr, (size_t)(nrows + 1) * sizeof(int64_t)));
+  CUDA_TRY(ctx, cudaMalloc(&d_indices, (size_t)std::max<int64_t>(nnz, 1) * sizeof(int64_t)));
+  CUDA_TRY(ctx, cudaMalloc(&d_planes, (size_t)std::max<int64_t>(nnz, 1) * nplanes * sizeof(double)));
+  CUDA_TRY(ctx, cudaMalloc(&d_bad, sizeof(int)));
+  CUDA_TRY(ctx, cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_indptr, indptr, (size_t)(nrows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (nnz > 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_indices, indices, (size_t)nnz * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    for (int j = 0; j < nplanes; ++j)
+      CUDA_TRY(ctx, cudaMemcpyAsync(d_planes + (size_t)j * nnz, planes[j], (size_t)nnz * sizeof(double),
+                                    cudaMemcpyHostToDevice, st));
+  }
+  int rc;
+  // SELL store
+  if ((rc = dev_alloc(ctx, A, &A->slice_ptr, (size_t)A->nslices + 1))) return rc;
+  if ((rc = dev_alloc(ctx, A, &A->slot_row, (size_t)(A->nslices * C)))) return rc;
+  if ((rc = dev_alloc(ctx, A, &A->slot_len, (size_t)(A->nslices * C)))) return rc;
+  if ((rc = dev_alloc(ctx, A, &A->scol, (size_t)A->sell_elems))) return rc;
+  if ((rc = dev_alloc(ctx, A, &A->sval, (size_t)A->sell_elems * nplanes))) return rc;
+  CUDA_TRY(ctx, cudaMemcpyAsync(A->slice_ptr, slice_ptr.data(), slice_ptr.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (A->nslices) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->slot_row, slot_row.data(), slot_row.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->slot_len, slot_len.data(), slot_len.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    const int64_t nslots = A->nslices * C;
+    build_sell_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(
+        nslots, C, A->slice_ptr, A->slot_row, A->slot_len, d_indptr, d_indices, d_planes, nplanes, nnz,
+        ncols, A->scol, A->sval, A->sell_elems, d_bad);
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  // long store
+  if (A->nlong) {
+    const int NS = A->cplx ? 4 : 1;
+    if ((rc = dev_alloc(ctx, A, &A->lrow, (size_t)A->nlong))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->lptr, (size_t)A->nlong + 1))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->lcol, (size_t)A->long_nnz))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->lval, (size_t)A->long_nnz * nplanes))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->chunk_row, (size_t)A->nchunks))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->chunk_first, (size_t)A->nlong + 1))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->partial, (size_t)A->nchunks * NS * K))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->counter, (size_t)A->nlong))) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->lrow, long_rows.data(), long_rows.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->lptr, lptr.data(), lptr.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->chunk_row, chunk_row.data(), chunk_row.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->chunk_first, chunk_first.data(), chunk_first.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemsetAsync(A->counter, 0, (size_t)A->nlong * sizeof(unsigned), st));
+    build_long_kernel<<<(unsigned)A->nlong, 256, 0, st>>>(A->lrow, A->lptr, d_indptr, d_indices, d_planes,
+                                                          nplanes, nnz, ncols, A->lcol, A->lval,
+                                                          A->long_nnz, d_bad);
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  int bad = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (bad) return fail(ctx, MPSG_E_RANGE, "csr_upload: column index outside [0, %lld)", (long long)ncols);
+  *out = holder.release();
+  return MPSG_OK;
+}
+
+void mpsg_csr_destroy(mpsg_csr* A) { free_csr(A); }
+
+int mpsg_csr_get_stats(const mpsg_csr* A, mpsg_csr_stats* o) {
+  if (!A || !o) return MPSG_E_ARG;
+  o->nrows = A->nrows;
+  o->ncols = A->ncols;
+  o->nnz = A->nnz;
+  o->K = A->K;
+  o->is_complex = A->cplx;
+  o->nslices = A->nslices;
+  o->sell_elems = A->sell_elems;
+  o->nlong = A->nlong;
+  o->long_nnz = A->long_nnz;
+  o->nchunks = A->nchunks;
+  o->device_bytes = A->device_bytes;
+  return MPSG_OK;
+}
+
+int mpsg_spmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_x, double* d_y,
+                  void* stream) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "spmv: matrix is complex, use mpsg_spmv_complex");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return launch_spmv(ctx, A, order, d_x, nullptr, d_y, nullptr, st);
+}
+
+int mpsg_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen, const double* x,
+              double* y) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (xlen != A->ncols) return fail(ctx, MPSG_E_DIM, "%s", dim_msg("spmv", xlen, A->ncols).c_str());
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "spmv: matrix is complex, use mpsg_spmv_complex");
+  const size_t xb = (size_t)A->ncols * A->K * sizeof(double), yb = (size_t)A->nrows * A->K * sizeof(double);
+  int rc;
+  if ((rc = ensure_scratch(ctx, 0, xb))) return rc;
+  if ((rc = ensure_scratch(ctx, 1, yb))) return rc;
+  cudaStream_t st = ctx->stream;
+  if (xb) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], x, xb, cudaMemcpyHostToDevice, st));
+  if ((rc = launch_spmv(ctx, A, order, ctx->dbuf[0], nullptr, ctx->dbuf[1], nullptr, st))) return rc;
+  if (yb) CUDA_TRY(ctx, cudaMemcpyAsync(y, ctx->dbuf[1], yb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MPSG_OK;
+}
+
+int mpsg_spmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_x_re,
+                          const double* d_x_im, double* d_y_re, double* d_y_im, void* stream) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (!A->cplx) return fail(ctx, MPSG_E_ARG, "spmv_complex: matrix is real");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return launch_spmv(ctx, A, order, d_x_re, d_x_im, d_y_re, d_y_im, st);
+}
+
+int mpsg_spmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen,
+                      const double* x_re, const double* x_im, double* y_re, double* y_im) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (!A->cplx) return fail(ctx, MPSG_E_ARG, "spmv_complex: matrix is real");
+  if (xlen != A->ncols) return fail(ctx, MPSG_E_DIM, "%s", dim_msg("spmv", xlen, A->ncols).c_str());
+  const size_t xb = (size_t)A->ncols * A->K * sizeof(double), yb = (size_t)A->nrows * A->K * sizeof(double);
+  int rc;
+  for (int s = 0; s < 4; ++s)
+    if ((rc = ensure_scratch(ctx, s, s < 2 ? xb : yb))) return rc;
+  cudaStream_t st = ctx->stream;
+  if (xb) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], x_re, xb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[1], x_im, xb, cudaMemcpyHostToDevice, st));
+  }
+  if ((rc = launch_spmv(ctx, A, order, ctx->dbuf[0], ctx->dbuf[1], ctx->dbuf[2], ctx->dbuf[3], st))) return rc;
+  if (yb) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(y_re, ctx->dbuf[2], yb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(y_im, ctx->dbuf[3], yb, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MPSG_OK;
+}
+
+int mpsg_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, const double* b,
+            const double* x0, const mpsg_cg_config* cfg, double* x_out, double* history,
+            int64_t history_cap, mpsg_cg_report* report) {
+  if (!ctx || !A || !cfg || !report || !b) return MPSG_E_ARG;
+  // SolverConfig::validate (krylov.hpp:69-75) and solver_init shape checks (:164-176)
+  if (!(cfg->rel_tol > 0.0) || !(cfg->abs_tol > 0.0))
+    return fail(ctx, MPSG_E_ARG, "solver: tolerances must be positive");
+  if (cfg->max_iters < 1) return fail(ctx, MPSG_E_ARG, "solver: max_iters must be at least 1");
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "solver: complex matrices are not supported by cg");
+  if (A->nrows != A->ncols)
+    return fail(ctx, MPSG_E_DIM, "solver: operator must be square, got %lldx%lld", (long long)A->nrows,
+                (long long)A->ncols);
+  if (blen != A->ncols) return fail(ctx, MPSG_E_DIM, "solver: rhs length does not match the operator");
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "cg: unknown order %d", order);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  switch (A->K) {
+    case 2: return run_cg<2>(ctx, A, order, b, x0, cfg, x_out, history, history_cap, report);
+    case 3: return run_cg<3>(ctx, A, order, b, x0, cfg, x_out, history, history_cap, report);
+    case 4: return run_cg<4>(ctx, A, order, b, x0, cfg, x_out, history, history_cap, report);
+  }
+  return fail(ctx, MPSG_E_ARG, "cg: unsupported K");
+}
+
+int mpsg_partition_rows(const int64_t* indptr, int64_t nrows, int parts, int64_t* bounds) {
+  // kernels.hpp:63-80: bounds[t] = first row with indptr >= total*t/parts
+  if (!indptr || !bounds || parts < 1) return MPSG_E_ARG;
+  for (int t = 0; t <= parts; ++t) bounds[t] = nrows;
+  bounds[0] = 0;
+  const int64_t total = indptr[nrows];
+  for (int t = 1; t < parts; ++t) {
+    const int64_t target = total * t / parts;
+    int64_t lo = bounds[t - 1], hi = nrows;
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (indptr[mid] < target)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    bounds[t] = lo;
+  }
+  return MPSG_OK;
+}
+
+uint64_t mpsg_checksum(int K, int64_t n, const double* v) {
+  uint64_t h = 14695981039346656037ull;
+  for (int64_t i = 0; i < n * K; ++i) {
+    uint64_t bits;
+    std::memcpy(&bits, v + i, 8);
+    for (int b = 0; b < 8; ++b) {
+      h ^= (bits >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+
+uint64_t mpsg_checksum_complex(int K, int64_t n, const double* re, const double* im) {
+  return mpsg_checksum(K, n, re) * 1099511628211ull ^ mpsg_checksum(K, n, im);
+}
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+// cg_kernels.cuh -- device-resident conjugate gradient (krylov.hpp:238-281).
+//
+// One CG iteration of the reference,
+//     q = A p;  sigma = <p,q>;  breakdown if tiny(sigma);  alpha = rho/sigma;
+//     x += alpha p;  r += (-alpha) q;  rho' = <r,r>;  |r| = sqrt(rho');
+//     record / stop tests;  beta = rho'/rho;  p = r + beta p;  rho = rho'
+// runs as four stream-ordered launches (SpMV, dot, fused x/r update + dot,
+// p update) that never return to the host: the scalar recurrences (MC divide,
+// sqrt, compare) and the stop tests run in the last block of each reduction
+// and write a device-side state word the next launches read.  The host polls
+// that word once per captured batch of iterations (CUDA graph).
+//
+// Dots use a fixed two-level tree (fixed grid, fixed per-thread strides,
+// fixed block tree, fixed partial order), so results do not depend on
+// scheduling; they are not the reference's sequential order (krylov.hpp:
+// 122-128), which is why CG parity is stated in iterations and residuals.
+#pragma once
+
+#include "mc_arith.cuh"
+
+namespace mpsg {
+
+constexpr int CG_RUNNING = -1;
+constexpr int DOT_THREADS = 256;
+constexpr int DOT_MAX_BLOCKS = 1024;
+
+// Device-side solver state (one per solve).
+template <int K>
+struct CgState {
+  MC<K> rho, sigma, alpha, beta, thr, bnorm, scratch;
+  int status;         // CG_RUNNING or mpsg_solver_status
+  int reason;         // 0 none, 1 <p,Ap> vanished, 2 non-finite residual
+  long long k;        // completed iterations
+  long long max_iters;
+  double rel_tol, abs_tol, divergence_cap, breakdown_floor;
+  double rhs_norm;
+  double true_residual;
+  double* history;    // [max_iters+1]
+  unsigned ticket;    // last-block arrival counter (self-resetting)
+};
+
+enum DotPost {
+  POST_BNORM = 0,  // bnorm = sqrt(<b,b>); threshold; caps
+  POST_R0 = 1,     // <r,r>: rho; history[0]; converged-at-start test
+  POST_SIGMA = 2,  // <p,q>: breakdown test; alpha
+  POST_RHO = 3,    // <r,r> after the update: record_step; beta; rho
+  POST_TRUE = 4    // ||b - A x||: final true residual
+};
+
+template <int K>
+MPSG_DI MC<K> block_reduce(MC<K> v, MC<K>* sh) {
+  // fixed xor tree inside each warp, then warp partials in warp order
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = add(v, shfl_xor(v, off));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  MC<K> s = sh[0];
+  if (threadIdx.x == 0)
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) s = add(s, sh[i]);
+  return s;  // valid in thread 0
+}
+
+// The scalar tail of every reduction, run by thread 0 of the last block.
+template <int K>
+MPSG_DI void cg_post(CgState<K>* st, int post, const MC<K>& d) {
+  if (post == POST_BNORM) {
+    MC<K> bn = sqrt_mc(d);
+    st->bnorm = bn;
+    // threshold = bnorm * rel_tol + abs_tol (krylov.hpp:185-186)
+    st->thr = add(mul_d(bn, st->rel_tol), from_double<K>(st->abs_tol));
+    st->rhs_norm = to_double(bn);
+    st->divergence_cap = 1e6 * st->rhs_norm + 1e6 * st->abs_tol;
+    st->breakdown_floor = 1e-3 * st->abs_tol;
+  } else if (post == POST_R0) {
+    MC<K> rn = sqrt_mc(d);
+    st->history[0] = to_double(rn);
+    st->rho = d;
+    st->k = 0;
+    if (less_equal(rn, st->thr)) {  // krylov.hpp:193-197
+      st->status = 0;
+    } else {
+      st->status = CG_RUNNING;
+    }
+  } else if (post == POST_SIGMA) {
+    st->sigma = d;
+    const double sd = to_double(d);
+    if (!finite(sd) || fabs(sd) < st->breakdown_floor) {  // krylov.hpp:250-254, :234
+      st->status = 2;
+      st->reason = 1;
+    } else {
+      st->alpha = divide(st->rho, d);
+    }
+  } else if (post == POST_RHO) {
+    const long long k = st->k + 1;
+    MC<K> rn = sqrt_mc(d);
+    const double rd = to_double(rn);
+    st->history[k] = rd;
+    st->k = k;
+    // record_step (krylov.hpp:205-213)
+    if (!finite(rd)) {
+      st->status = 2;
+      st->reason = 2;
+    } else if (less_equal(rn, st->thr)) {
+      st->status = 0;
+    } else if (rd > st->divergence_cap) {
+      st->status = 3;
+    } else {
+      st->beta = divide(d, st->rho);
+      st->rho = d;
+      if (k >= st->max_iters) st->status = 1;
+    }
+  } else if (post == POST_TRUE) {
+    st->true_residual = to_double(sqrt_mc(d));
+  }
+}
+
+// Generic reduction kernel body.  MODE selects the per-element work:
+//   0: d += u_i * v_i                                   (dots)
+//   1: x_i += alpha p_i; r_i += (-alpha) q_i; d += r_i r_i (axpy pair + dot)
+//   2: w_i = b_i - w_i; d += w_i w_i                    (true residual)
+template <int K, int MODE>
+__global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, int post, int64_t n,
+                                                                const double* u, const double* v,
+                                                                double* x, double* r, double* partial,
+                                                                int gate) {
+  __shared__ MC<K> sh[DOT_THREADS / 32];
+  __shared__ bool last;
+  if (gate && st->status != CG_RUNNING) return;
+  const int G = gridDim.x;
+  const int64_t seg = (n + G - 1) / G;
+  const int64_t lo = (int64_t)blockIdx.x * seg;
+  const int64_t hi = (lo + seg < n) ? lo + seg : n;
+  MC<K> acc = zero<K>();
+  if constexpr (MODE == 0) {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS)
+      acc = add(acc, mul(load_aos_rw<K>(u, i), load_aos_rw<K>(v, i)));
+  } else if constexpr (MODE == 1) {
+    // u = p, v = q; x, r updated in place (krylov.hpp:256-257: axpy = y + alpha*x)
+    const MC<K> alpha = st->alpha;
+    const MC<K> malpha = negate(alpha);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) {
+      MC<K> xi = add(load_aos_rw<K>(x, i), mul(alpha, load_aos_rw<K>(u, i)));
+      MC<K> ri = add(load_aos_rw<K>(r, i), mul(malpha, load_aos_rw<K>(v, i)));
+      store_aos<K>(x, i, xi);
+      store_aos<K>(r, i, ri);
+      acc = add(acc, mul(ri, ri));
+    }
+  } else {
+    // u = b, x = A x (overwritten with b - A x)
+    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) {
+      MC<K> w = sub(load_aos_rw<K>(u, i), load_aos_rw<K>(x, i));
+      store_aos<K>(x, i, w);
+      acc = add(acc, mul(w, w));
+    }
+  }
+  MC<K> bsum = block_reduce(acc, sh);
+  if (threadIdx.x == 0) {
+    double* pp = partial + (int64_t)blockIdx.x * K;
+#pragma unroll
+    for (int j = 0; j < K; ++j) __stcg(pp + j, bsum.c[j]);
+    __threadfence();
+    last = (atomicAdd(&st->ticket, 1u) == (unsigned)(G - 1));
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // last block: fixed-order sum of the G partials (thread t takes a
+  // contiguous run, then the block tree), then the scalar step.
+  const int per = (G + DOT_THREADS - 1) / DOT_THREADS;
+  MC<K> s = zero<K>();
+  for (int i = threadIdx.x * per; i < (threadIdx.x + 1) * per && i < G; ++i) {
+    MC<K> pv;
+#pragma unroll
+    for (int j = 0; j < K; ++j) pv.c[j] = __ldcg(partial + (int64_t)i * K + j);
+    s = add(s, pv);
+  }
+  __syncthreads();
+  MC<K> tot = block_reduce(s, sh);
+  if (threadIdx.x == 0) {
+    st->ticket = 0u;
+    cg_post(st, post, tot);
+  }
+}
+
+// p = r + beta p (krylov.hpp:272)
+template <int K>
+__global__ void __launch_bounds__(256) cg_update_p_kernel(const CgState<K>* st, int64_t n,
+                                                          const double* r, double* p) {
+  if (st->status != CG_RUNNING) return;
+  const MC<K> beta = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(beta, load_aos_rw<K>(p, i))));
+}
+
+// Initial state: r = b (or b - A x0 computed by the caller), p = r.
+template <int K>
+__global__ void cg_init_state_kernel(CgState<K>* st, double rel_tol, double abs_tol,
+                                     long long max_iters, double* history) {
+  st->status = CG_RUNNING;
+  st->reason = 0;
+  st->k = 0;
+  st->max_iters = max_iters;
+  st->rel_tol = rel_tol;
+  st->abs_tol = abs_tol;
+  st->history = history;
+  st->ticket = 0u;
+  st->true_residual = 0.0;
+}
+
+}  // namespace mpsg

@@ -1,0 +1,97 @@
+// internal.h -- host-side internals shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/mpsg.h"
+#include "layout.h"
+
+using mpsg::LongView;
+using mpsg::SellView;
+
+struct mpsg_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // current (own or caller's)
+  cudaStream_t aux = nullptr;     // long-row kernels run here, forked/joined by events
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::string err;
+  // scratch for host-pointer calls
+  double* dbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t dcap[4] = {0, 0, 0, 0};
+  int64_t long_threshold = 256;
+  int64_t sigma = 16384;
+  int64_t fast_chunk = 2048;
+};
+
+struct mpsg_csr {
+  int K = 2;
+  bool cplx = false;
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  // SELL store
+  int C = 32;
+  int64_t nslices = 0, sell_elems = 0;
+  int64_t* slice_ptr = nullptr;
+  int* slot_row = nullptr;
+  int* slot_len = nullptr;
+  int* scol = nullptr;
+  double* sval = nullptr;
+  // long store
+  int64_t nlong = 0, long_nnz = 0, nchunks = 0, chunk = 2048;
+  int* lrow = nullptr;
+  int64_t* lptr = nullptr;
+  int* lcol = nullptr;
+  double* lval = nullptr;
+  int* chunk_row = nullptr;
+  int* chunk_first = nullptr;
+  double* partial = nullptr;
+  unsigned* counter = nullptr;
+  int64_t device_bytes = 0;
+
+  SellView sell() const {
+    return SellView{(int)nslices, C, slice_ptr, slot_row, slot_len, scol, sval, sell_elems};
+  }
+  LongView lng() const {
+    return LongView{(int)nlong, lrow, lptr, lcol, lval, long_nnz, (int)chunk, (int)nchunks,
+                    chunk_row, chunk_first, partial, counter};
+  }
+};
+
+namespace mpsg {
+
+inline int fail(mpsg_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define CUDA_TRY(ctx, call)                                                                   \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? MPSG_E_OOM : MPSG_E_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+// SpMV launch for one (K, complex) instantiation (spmv_k{2,3,4}.cu).
+template <int K, bool CPLX>
+int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre,
+                  const double* xim, double* yre, double* yim, cudaStream_t st);
+// Dispatch over K / complex (capi.cu).
+int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
+                double* yre, double* yim, cudaStream_t st);
+// Device CG driver for one K (cg_k{2,3,4}.cu).
+template <int K>
+int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, const double* x0,
+           const mpsg_cg_config* cfg, double* x_out, double* history, int64_t history_cap,
+           mpsg_cg_report* rep);
+
+}  // namespace mpsg

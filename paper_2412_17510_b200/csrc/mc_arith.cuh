@@ -1,0 +1,429 @@
+// mc_arith.cuh -- sm_100a device multi-component (DD/TD/QD) arithmetic.
+//
+// Op-for-op restatement of the reference arithmetic so the deterministic
+// kernels reproduce its bits (paths under /root/reference/proj/include/mps/):
+//   eft.hpp:26-80        quick_two_sum_raw, two_sum, two_prod_fma, three_sum(2)
+//   multicomp.hpp:43-78  renorm_n<K,N> (branchy forward collect kept exactly)
+//   multicomp.hpp:80-215 DD cores, QD sloppy prenorms, TD-as-zero-extended-QD
+//   multicomp.hpp:225-335 add / mul / mul_by_double / sub / divide / sqrt /
+//                         to_double / compare
+// Every arithmetic step is an explicit round-to-nearest intrinsic
+// (__dadd_rn, __dsub_rn, __dmul_rn, __fma_rn), so no compiler flag can contract
+// or reassociate them; fma appears only where the reference calls std::fma
+// (eft.hpp:57, multicomp.hpp:106).  Values live in registers as MC<K>
+// (K doubles, magnitude-decreasing).
+#pragma once
+
+#include <cstdint>
+
+namespace mpsg {
+
+template <int K>
+struct MC {
+  double c[K];
+};
+
+#define MPSG_DI __device__ __forceinline__
+
+MPSG_DI double dadd(double a, double b) { return __dadd_rn(a, b); }
+MPSG_DI double dsub(double a, double b) { return __dsub_rn(a, b); }
+MPSG_DI double dmul(double a, double b) { return __dmul_rn(a, b); }
+MPSG_DI double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// Bit tests on the integer pipe instead of DSETP on the fp64 pipe.
+// x != 0.0 (false for +-0, true for NaN), multicomp.hpp:68.
+MPSG_DI bool nonzero(double x) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b << 1) != 0ull;
+}
+// std::isfinite, multicomp.hpp:47.
+MPSG_DI bool finite(double x) {
+  return (__double2hiint(x) & 0x7ff00000) != 0x7ff00000;
+}
+
+// ---------------------------------------------------------------- EFTs --
+MPSG_DI void qts(double a, double b, double& s, double& e) {  // eft.hpp:26-30
+  double ss = dadd(a, b);
+  e = dsub(b, dsub(ss, a));
+  s = ss;
+}
+MPSG_DI void two_sum(double a, double b, double& s, double& e) {  // eft.hpp:34-41
+  double ss = dadd(a, b);
+  double v = dsub(ss, a);
+  e = dadd(dsub(a, dsub(ss, v)), dsub(b, v));
+  s = ss;
+}
+MPSG_DI void two_prod(double a, double b, double& p, double& e) {  // eft.hpp:53-59
+  double pp = dmul(a, b);
+  e = dfma(a, b, -pp);
+  p = pp;
+}
+MPSG_DI void three_sum(double& a, double& b, double& c) {  // eft.hpp:63-71
+  double t1, t2, s1, t3, s2, s3;
+  two_sum(a, b, t1, t2);
+  two_sum(c, t1, s1, t3);
+  two_sum(t2, t3, s2, s3);
+  a = s1;
+  b = s2;
+  c = s3;
+}
+MPSG_DI void three_sum2(double& a, double& b, double c) {  // eft.hpp:74-80
+  double t1, t2, s1, t3;
+  two_sum(a, b, t1, t2);
+  two_sum(c, t1, s1, t3);
+  a = s1;
+  b = dadd(t2, t3);
+}
+
+// ------------------------------------------------------------ renorm_n --
+// multicomp.hpp:43-78.  t[] is taken by value in registers; the forward
+// collect's runtime slot index is expressed with selects so nothing spills
+// to local memory, yielding the same values as the reference's branches.
+template <int K, int N>
+MPSG_DI MC<K> renorm(double (&t)[N]) {
+  MC<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) r.c[i] = 0.0;
+  if (!finite(t[0])) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s = dadd(s, t[i]);
+    r.c[0] = s;
+    return r;
+  }
+  double s = t[N - 1];
+#pragma unroll
+  for (int i = N - 2; i >= 0; --i) {
+    double hi, lo;
+    qts(t[i], s, hi, lo);
+    s = hi;
+    t[i + 1] = lo;
+  }
+  t[0] = s;
+  int k = 0;
+  s = t[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) {
+    if (k == K - 1) {
+      s = dadd(s, t[i]);
+    } else {
+      double hi, lo;
+      qts(s, t[i], hi, lo);
+      if (nonzero(lo)) {
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j)
+          if (k == j) r.c[j] = hi;
+        ++k;
+        s = lo;
+      } else {
+        s = hi;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (k == j) r.c[j] = s;
+  return r;
+}
+
+// ------------------------------------------------------------ DD cores --
+MPSG_DI MC<2> dd_add(const MC<2>& x, const MC<2>& y) {  // multicomp.hpp:80-88
+  double s, e;
+  two_sum(x.c[0], y.c[0], s, e);
+  double w = dadd(x.c[1], y.c[1]);
+  e = dadd(e, w);
+  MC<2> r;
+  qts(s, e, r.c[0], r.c[1]);
+  return r;
+}
+MPSG_DI MC<2> dd_mul(const MC<2>& x, const MC<2>& y) {  // multicomp.hpp:90-100
+  double p1, p2;
+  two_prod(x.c[0], y.c[0], p1, p2);
+  double w1 = dmul(x.c[0], y.c[1]);
+  double w2 = dmul(x.c[1], y.c[0]);
+  double w3 = dadd(w1, w2);
+  p2 = dadd(p2, w3);
+  MC<2> r;
+  qts(p1, p2, r.c[0], r.c[1]);
+  return r;
+}
+MPSG_DI MC<2> dd_mul_d(const MC<2>& x, double y) {  // multicomp.hpp:102-110
+  double p1, p2;
+  two_prod(x.c[0], y, p1, p2);
+  p2 = dfma(x.c[1], y, p2);
+  MC<2> r;
+  qts(p1, p2, r.c[0], r.c[1]);
+  return r;
+}
+
+// ----------------------------------------------------- QD/TD prenorms --
+// multicomp.hpp:112-132
+MPSG_DI void qd_add_prenorm(const double* x, const double* y, double* out) {
+  double s0, t0, s1, t1, s2, t2, s3, t3;
+  two_sum(x[0], y[0], s0, t0);
+  two_sum(x[1], y[1], s1, t1);
+  two_sum(x[2], y[2], s2, t2);
+  two_sum(x[3], y[3], s3, t3);
+  double s1b, t0b;
+  two_sum(s1, t0, s1b, t0b);
+  s1 = s1b;
+  t0 = t0b;
+  three_sum(s2, t0, t1);
+  three_sum2(s3, t0, t2);
+  t0 = dadd(dadd(t0, t1), t3);
+  out[0] = s0;
+  out[1] = s1;
+  out[2] = s2;
+  out[3] = s3;
+  out[4] = t0;
+}
+// multicomp.hpp:134-163
+MPSG_DI void qd_mul_prenorm(const double* a, const double* b, double* out) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
+  two_prod(a[0], b[0], p0, q0);
+  two_prod(a[0], b[1], p1, q1);
+  two_prod(a[1], b[0], p2, q2);
+  two_prod(a[0], b[2], p3, q3);
+  two_prod(a[1], b[1], p4, q4);
+  two_prod(a[2], b[0], p5, q5);
+  three_sum(p1, p2, q0);
+  three_sum(p2, q1, q2);
+  three_sum(p3, p4, p5);
+  double s0, t0, s1, t1;
+  two_sum(p2, p3, s0, t0);
+  two_sum(q1, p4, s1, t1);
+  double s2 = dadd(q2, p5);
+  double s1b, t0b;
+  two_sum(s1, t0, s1b, t0b);
+  s1 = s1b;
+  s2 = dadd(s2, dadd(t0b, t1));
+  // multicomp.hpp:156, strictly left to right with separate multiplies
+  double tail = dadd(dmul(a[0], b[3]), dmul(a[1], b[2]));
+  tail = dadd(tail, dmul(a[2], b[1]));
+  tail = dadd(tail, dmul(a[3], b[0]));
+  tail = dadd(tail, q0);
+  tail = dadd(tail, q3);
+  tail = dadd(tail, q4);
+  tail = dadd(tail, q5);
+  s1 = dadd(s1, tail);
+  out[0] = p0;
+  out[1] = p1;
+  out[2] = s0;
+  out[3] = s1;
+  out[4] = s2;
+}
+// multicomp.hpp:165-183
+MPSG_DI void qd_mul_d_prenorm(const double* a, double b, double* out) {
+  double p0, q0, p1, q1, p2, q2;
+  two_prod(a[0], b, p0, q0);
+  two_prod(a[1], b, p1, q1);
+  two_prod(a[2], b, p2, q2);
+  double p3 = dmul(a[3], b);
+  double s1, s2;
+  two_sum(q0, p1, s1, s2);
+  three_sum(s2, q1, p2);
+  three_sum2(q1, p2, p3);
+  out[0] = p0;
+  out[1] = s1;
+  out[2] = s2;
+  out[3] = q1;
+  out[4] = dadd(q2, p2);
+}
+// multicomp.hpp:185-199
+MPSG_DI void td_mul_d_prenorm(const double* a, double b, double* out) {
+  double p0, q0, p1, q1, p2, q2;
+  two_prod(a[0], b, p0, q0);
+  two_prod(a[1], b, p1, q1);
+  two_prod(a[2], b, p2, q2);
+  double s1, s2;
+  two_sum(q0, p1, s1, s2);
+  three_sum(s2, q1, p2);
+  out[0] = p0;
+  out[1] = s1;
+  out[2] = s2;
+  out[3] = dadd(q2, p2);
+}
+
+// ------------------------------------------------ public MC operations --
+// multicomp.hpp:225-277 (add / mul / mul_by_double per width)
+MPSG_DI MC<2> add(const MC<2>& x, const MC<2>& y) { return dd_add(x, y); }
+MPSG_DI MC<2> mul(const MC<2>& x, const MC<2>& y) { return dd_mul(x, y); }
+MPSG_DI MC<2> mul_d(const MC<2>& x, double y) { return dd_mul_d(x, y); }
+
+MPSG_DI MC<3> add(const MC<3>& x, const MC<3>& y) {  // multicomp.hpp:243-247, :203-207
+  double xe[4] = {x.c[0], x.c[1], x.c[2], 0.0};
+  double ye[4] = {y.c[0], y.c[1], y.c[2], 0.0};
+  double t[5];
+  qd_add_prenorm(xe, ye, t);
+  return renorm<3, 5>(t);
+}
+MPSG_DI MC<3> mul(const MC<3>& x, const MC<3>& y) {  // multicomp.hpp:249-253, :210-214
+  double xe[4] = {x.c[0], x.c[1], x.c[2], 0.0};
+  double ye[4] = {y.c[0], y.c[1], y.c[2], 0.0};
+  double t[5];
+  qd_mul_prenorm(xe, ye, t);
+  return renorm<3, 5>(t);
+}
+MPSG_DI MC<3> mul_d(const MC<3>& x, double y) {  // multicomp.hpp:255-259
+  double t[4];
+  td_mul_d_prenorm(x.c, y, t);
+  return renorm<3, 4>(t);
+}
+MPSG_DI MC<4> add(const MC<4>& x, const MC<4>& y) {  // multicomp.hpp:261-265
+  double t[5];
+  qd_add_prenorm(x.c, y.c, t);
+  return renorm<4, 5>(t);
+}
+MPSG_DI MC<4> mul(const MC<4>& x, const MC<4>& y) {  // multicomp.hpp:267-271
+  double t[5];
+  qd_mul_prenorm(x.c, y.c, t);
+  return renorm<4, 5>(t);
+}
+MPSG_DI MC<4> mul_d(const MC<4>& x, double y) {  // multicomp.hpp:273-277
+  double t[5];
+  qd_mul_d_prenorm(x.c, y, t);
+  return renorm<4, 5>(t);
+}
+
+template <int K>
+MPSG_DI MC<K> zero() {
+  MC<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) r.c[i] = 0.0;
+  return r;
+}
+template <int K>
+MPSG_DI MC<K> from_double(double v) {  // MultiComponent(double), multicomp.hpp:23
+  MC<K> r = zero<K>();
+  r.c[0] = v;
+  return r;
+}
+template <int K>
+MPSG_DI MC<K> negate(const MC<K>& x) {  // multicomp.hpp:279-284
+  MC<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) r.c[i] = -x.c[i];
+  return r;
+}
+template <int K>
+MPSG_DI MC<K> sub(const MC<K>& x, const MC<K>& y) {  // multicomp.hpp:286-289
+  return add(x, negate(y));
+}
+// multicomp.hpp:291-302: K+1 quotient digits, then renorm<K>(q)
+template <int K>
+MPSG_DI MC<K> divide(const MC<K>& a, const MC<K>& b) {
+  double q[K + 1];
+  MC<K> r = a;
+#pragma unroll
+  for (int i = 0; i <= K; ++i) {
+    q[i] = __ddiv_rn(r.c[0], b.c[0]);
+    if (i < K) r = sub(r, mul_d(b, q[i]));
+  }
+  if constexpr (K == 2) {
+    // renorm<2> = renorm_n<2,3>
+    return renorm<2, 3>(q);
+  } else {
+    return renorm<K, K + 1>(q);
+  }
+}
+// multicomp.hpp:304-322: Newton on 1/sqrt(a), then one multiply-back step
+template <int K>
+MPSG_DI MC<K> sqrt_mc(const MC<K>& a) {
+  if (a.c[0] == 0.0) return zero<K>();
+  if (a.c[0] < 0.0 || a.c[0] != a.c[0]) return from_double<K>(__longlong_as_double(0x7ff8000000000000ll));
+  MC<K> x = from_double<K>(__ddiv_rn(1.0, __dsqrt_rn(a.c[0])));
+  const MC<K> one = from_double<K>(1.0);
+  const int iters = (K == 4) ? 3 : 2;
+  for (int i = 0; i < iters; ++i) {
+    MC<K> e = sub(one, mul(a, mul(x, x)));
+    x = add(x, mul_d(mul(x, e), 0.5));
+  }
+  MC<K> r = mul(a, x);
+  r = add(r, mul_d(mul(sub(a, mul(r, r)), x), 0.5));
+  return r;
+}
+// multicomp.hpp:329-335
+template <int K>
+MPSG_DI double to_double(const MC<K>& x) {
+  double s = x.c[K - 1];
+#pragma unroll
+  for (int i = K - 2; i >= 0; --i) s = dadd(x.c[i], s);
+  return s;
+}
+// multicomp.hpp:342-351 (-2 when unordered)
+template <int K>
+MPSG_DI int compare(const MC<K>& x, const MC<K>& y) {
+  if (x.c[0] != x.c[0] || y.c[0] != y.c[0]) return -2;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    if (x.c[i] < y.c[i]) return -1;
+    if (x.c[i] > y.c[i]) return 1;
+  }
+  return 0;
+}
+template <int K>
+MPSG_DI bool less_equal(const MC<K>& x, const MC<K>& y) {  // multicomp.hpp:390-393
+  int c = compare(x, y);
+  return c == 0 || c == -1;
+}
+
+// -------------------------------------------------------- memory helpers --
+template <int K>
+MPSG_DI MC<K> load_aos(const double* __restrict__ p, int64_t i) {
+  MC<K> r;
+  const double* q = p + i * K;
+  if constexpr (K == 2) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(q));
+    r.c[0] = v.x;
+    r.c[1] = v.y;
+  } else if constexpr (K == 4) {
+    double2 v0 = __ldg(reinterpret_cast<const double2*>(q));
+    double2 v1 = __ldg(reinterpret_cast<const double2*>(q) + 1);
+    r.c[0] = v0.x;
+    r.c[1] = v0.y;
+    r.c[2] = v1.x;
+    r.c[3] = v1.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) r.c[j] = __ldg(q + j);
+  }
+  return r;
+}
+// Plain (coherent) loads for vectors written earlier in the same launch
+// sequence without a kernel boundary guarantee of read-only-ness.
+template <int K>
+MPSG_DI MC<K> load_aos_rw(const double* p, int64_t i) {
+  MC<K> r;
+#pragma unroll
+  for (int j = 0; j < K; ++j) r.c[j] = p[i * K + j];
+  return r;
+}
+template <int K>
+MPSG_DI void store_aos(double* __restrict__ p, int64_t i, const MC<K>& v) {
+  double* q = p + i * K;
+  if constexpr (K == 2) {
+    *reinterpret_cast<double2*>(q) = make_double2(v.c[0], v.c[1]);
+  } else if constexpr (K == 4) {
+    reinterpret_cast<double2*>(q)[0] = make_double2(v.c[0], v.c[1]);
+    reinterpret_cast<double2*>(q)[1] = make_double2(v.c[2], v.c[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) q[j] = v.c[j];
+  }
+}
+template <int K>
+MPSG_DI MC<K> shfl_xor(const MC<K>& v, int mask) {
+  MC<K> r;
+#pragma unroll
+  for (int j = 0; j < K; ++j) r.c[j] = __shfl_xor_sync(0xffffffffu, v.c[j], mask);
+  return r;
+}
+template <int K>
+MPSG_DI MC<K> shfl(const MC<K>& v, int src, unsigned mask = 0xffffffffu) {
+  MC<K> r;
+#pragma unroll
+  for (int j = 0; j < K; ++j) r.c[j] = __shfl_sync(mask, v.c[j], src);
+  return r;
+}
+
+}  // namespace mpsg
