@@ -36,7 +36,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpsg.so")
+LIB_PATH = os.environ.get("MPSG_LIB") or os.path.join(_HERE, "libmpsg.so")
 
 ORDER_SCALAR, ORDER_LANE4, ORDER_FAST = 0, 1, 2
 E_OK, E_DIM, E_RANGE, E_CUDA, E_NCCL, E_OOM, E_ARG, E_STRUCT = range(8)

@@ -147,6 +147,18 @@ int mpsg_ctx_create(int device, mpsg_ctx** out) {
     return MPSG_E_CUDA;
   }
   ctx->stream = ctx->own_stream;
+  {
+    // persisting L2 set-aside for the gathered vector (see launch_win).  Off
+    // by default: measured slower on B200 for every config (profiles/
+    // r01b_l2_persist.txt); MPSG_L2_PERSIST=1 turns it on.
+    const char* env = std::getenv("MPSG_L2_PERSIST");
+    int maxp = 0;
+    if (env && env[0] == '1' &&
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess && maxp > 0 &&
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) == cudaSuccess)
+      ctx->persist_max = (size_t)maxp;
+    cudaGetLastError();
+  }
   if (const char* s = std::getenv("MPSG_LONG_THRESHOLD")) ctx->long_threshold = std::atoll(s);
   if (const char* s = std::getenv("MPSG_SIGMA")) ctx->sigma = std::atoll(s);
   if (const char* s = std::getenv("MPSG_FAST_CHUNK")) ctx->fast_chunk = std::atoll(s);

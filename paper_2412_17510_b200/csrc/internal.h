@@ -23,6 +23,11 @@ struct mpsg_ctx {
   // scratch for host-pointer calls
   double* dbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t dcap[4] = {0, 0, 0, 0};
+  // L2 residency for the gathered vector: launches carry an access-policy
+  // window over x (persisting) so the streamed matrix (evict-first loads)
+  // does not push x out of L2.  persist_max = the device's persisting-L2
+  // capacity (0: unsupported / disabled by MPSG_L2_PERSIST=0).
+  size_t persist_max = 0;
   int64_t long_threshold = 256;
   int64_t sigma = 16384;
   int64_t fast_chunk = 2048;
@@ -80,6 +85,32 @@ inline int fail(mpsg_ctx* ctx, int code, const char* fmt, ...) {
       return fail(ctx, e_ == cudaErrorMemoryAllocation ? MPSG_E_OOM : MPSG_E_CUDA, "%s: %s (%s:%d)", \
                   #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
   } while (0)
+
+// Launch `kern` with an L2 access-policy window over [win, win+win_bytes)
+// when the context enables it (the window travels with the launch, so it is
+// captured into CUDA graphs too).
+template <class... KArgs, class... Args>
+cudaError_t launch_win(const mpsg_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, const void* win, size_t win_bytes, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (ctx->persist_max > 0 && win && win_bytes > 0) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(win);
+    attr[0].val.accessPolicyWindow.num_bytes = win_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio =
+        win_bytes <= ctx->persist_max ? 1.0f : (float)ctx->persist_max / (float)win_bytes;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // SpMV launch for one (K, complex) instantiation (spmv_k{2,3,4}.cu).
 template <int K, bool CPLX>

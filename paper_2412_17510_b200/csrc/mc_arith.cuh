@@ -76,15 +76,54 @@ MPSG_DI void three_sum2(double& a, double& b, double c) {  // eft.hpp:74-80
 }
 
 // ------------------------------------------------------------ renorm_n --
-// multicomp.hpp:43-78.  t[] is taken by value in registers; the forward
-// collect's runtime slot index is expressed with selects so nothing spills
-// to local memory, yielding the same values as the reference's branches.
+// multicomp.hpp:43-78.  t[] is taken by value in registers.
+//
+// The forward collect emits a component whenever QuickTwoSum leaves a
+// nonzero low part.  On full-precision data every one of the first K-1 steps
+// emits (the "common path": K-1 QuickTwoSums, then plain adds), so that path
+// is computed straight-line and only if one of its low parts is zero does the
+// general collect below run -- a warp-uniform branch on uniform data that
+// yields exactly the values of the reference's loop either way.
+// Zero tests use integer ops on the bit pattern (x != 0.0, true for NaN).
+MPSG_DI bool nonzero_i(double x) {
+  return ((__double2hiint(x) & 0x7fffffff) | __double2loint(x)) != 0;
+}
+
+template <int K, int N>
+MPSG_DI void renorm_general(double (&t)[N], MC<K>& r) {
+#pragma unroll
+  for (int i = 0; i < K; ++i) r.c[i] = 0.0;
+  int k = 0;
+  double s = t[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) {
+    if (k == K - 1) {
+      s = dadd(s, t[i]);
+    } else {
+      double hi, lo;
+      qts(s, t[i], hi, lo);
+      if (nonzero_i(lo)) {
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j)
+          if (k == j) r.c[j] = hi;
+        ++k;
+        s = lo;
+      } else {
+        s = hi;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (k == j) r.c[j] = s;
+}
+
 template <int K, int N>
 MPSG_DI MC<K> renorm(double (&t)[N]) {
   MC<K> r;
-#pragma unroll
-  for (int i = 0; i < K; ++i) r.c[i] = 0.0;
   if (!finite(t[0])) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) r.c[i] = 0.0;
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) s = dadd(s, t[i]);
@@ -100,29 +139,21 @@ MPSG_DI MC<K> renorm(double (&t)[N]) {
     t[i + 1] = lo;
   }
   t[0] = s;
-  int k = 0;
-  s = t[0];
+  // common path
+  bool ok = true;
 #pragma unroll
-  for (int i = 1; i < N; ++i) {
-    if (k == K - 1) {
-      s = dadd(s, t[i]);
-    } else {
-      double hi, lo;
-      qts(s, t[i], hi, lo);
-      if (nonzero(lo)) {
-#pragma unroll
-        for (int j = 0; j < K - 1; ++j)
-          if (k == j) r.c[j] = hi;
-        ++k;
-        s = lo;
-      } else {
-        s = hi;
-      }
-    }
+  for (int i = 1; i < K; ++i) {
+    double hi, lo;
+    qts(s, t[i], hi, lo);
+    r.c[i - 1] = hi;
+    s = lo;
+    ok = ok && nonzero_i(lo);
   }
 #pragma unroll
-  for (int j = 0; j < K; ++j)
-    if (k == j) r.c[j] = s;
+  for (int i = K; i < N; ++i) s = dadd(s, t[i]);
+  r.c[K - 1] = s;
+  if (__builtin_expect(ok, 1)) return r;
+  renorm_general<K, N>(t, r);
   return r;
 }
 

@@ -3,19 +3,27 @@
 #include "internal.h"
 #include "spmv_kernels.cuh"
 
+#ifndef MPSG_FAST_COMPLEX_ORDER
+#define MPSG_FAST_COMPLEX_ORDER ORDER_SCALAR
+#endif
+
 namespace mpsg {
 
 template <int K, bool CPLX>
 int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre,
                   const double* xim, double* yre, double* yim, cudaStream_t st) {
   const bool has_long = A->nlong > 0;
+  // x (re, then im for complex: one window over the first, the hotter, is
+  // all a launch can carry) stays L2-resident while the matrix streams
+  const size_t xb = (size_t)A->ncols * K * sizeof(double);
   if (has_long) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     LongView L = A->lng();
     if (order == ORDER_FAST) {
       const int blocks = (int)((A->nchunks + 3) / 4);
-      long_fast_kernel<K, CPLX><<<blocks, 128, 0, ctx->aux>>>(L, xre, xim, yre, yim);
+      CUDA_TRY(ctx, launch_win(ctx, long_fast_kernel<K, CPLX>, blocks, 128, 0, ctx->aux, xre, xb, L, xre, xim,
+                               yre, yim));
     } else {
       constexpr int CH = CPLX ? 256 : 512;
       const size_t smem = (size_t)CH * (CPLX ? 4 : 1) * sizeof(MC<K>);
@@ -30,16 +38,26 @@ int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre
   if (A->nslices > 0) {
     const int blocks = (int)((A->nslices + 3) / 4);
     SellView S = A->sell();
+    // Short rows: ORDER_FAST runs them in the reference's lanes-off order
+    // (bit-exact with lanes off, so trivially inside the fast-mode bound) --
+    // the faster of the two exact orders on B200 for every K
+    // (profiles/r01b_variants.txt); only long rows are reordered.
+    const int sorder = order == ORDER_FAST ? ORDER_SCALAR : order;
     if constexpr (!CPLX) {
-      if (order == ORDER_SCALAR)
-        sell_real_kernel<K, ORDER_SCALAR><<<blocks, 128, 0, st>>>(S, xre, yre);
+      if (sorder == ORDER_SCALAR)
+        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_SCALAR>, blocks, 128, 0, st, xre, xb, S, xre, yre));
+      else if constexpr (K == 2)
+        CUDA_TRY(ctx, launch_win(ctx, sell_real_lane4_lat_kernel<K>, blocks, 128, 0, st, xre, xb, S, xre, yre));
       else
-        sell_real_kernel<K, ORDER_LANE4><<<blocks, 128, 0, st>>>(S, xre, yre);
+        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_LANE4>, blocks, 128, 0, st, xre, xb, S, xre, yre));
     } else {
-      if (order == ORDER_SCALAR)
-        sell_complex_kernel<K, ORDER_SCALAR><<<blocks, 128, 0, st>>>(S, xre, xim, yre, yim);
+      const int corder = order == ORDER_FAST ? MPSG_FAST_COMPLEX_ORDER : order;
+      if (corder == ORDER_SCALAR)
+        CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_SCALAR>, blocks, 128, 0, st, xre, xb, S, xre,
+                                 xim, yre, yim));
       else
-        sell_complex_kernel<K, ORDER_LANE4><<<blocks, 128, 0, st>>>(S, xre, xim, yre, yim);
+        CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_LANE4>, blocks, 128, 0, st, xre, xb, S, xre,
+                                 xim, yre, yim));
     }
     CUDA_TRY(ctx, cudaGetLastError());
   }

@@ -44,11 +44,117 @@ MPSG_DI MC<K> load_planes_stream(const double* __restrict__ val, int64_t stride,
 }
 
 // ---------------------------------------------------------------------------
+// Row-sum building blocks for the SELL kernels.
+// ---------------------------------------------------------------------------
+// Lane chains evaluated concurrently in the LANE4 order (see lane4_row):
+// 2 for DD (latency-bound: more loads in flight), 1 for TD/QD (fp64-bound:
+// fewer live registers, more resident warps).  Measured on B200 in
+// profiles/r01b_chain_variants.txt.
+#ifndef MPSG_SELL_PAR_DD
+#define MPSG_SELL_PAR_DD 2
+#endif
+#define MPSG_SELL_PAR(K) ((K) == 2 ? MPSG_SELL_PAR_DD : 1)
+#ifdef MPSG_SELL_MINB
+#define MPSG_SELL_LB __launch_bounds__(128, MPSG_SELL_MINB)
+#else
+#define MPSG_SELL_LB __launch_bounds__(128)
+#endif
+
+// One product term of slot-row element k (matrix operand first, kernels.hpp:52-54).
+template <int K>
+MPSG_DI MC<K> sell_term(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
+                        const double* __restrict__ x, int k) {
+  const int64_t e = (int64_t)k * 32;
+  return mul(load_planes_stream<K>(vp, st, e), load_aos<K>(x, __ldcs(cp + e)));
+}
+
+// LANE4 order with the four lane chains evaluated P at a time.  Chain j
+// accumulates elements j, j+4, ... of the row's whole 4-groups; the lane
+// combine s = (((0 + L0) + L1) + L2) + L3 is folded in as soon as a chain is
+// complete, which is the reference's order (kernels.hpp:108-115) -- only the
+// schedule differs, so fewer accumulators are live at once (P*K doubles
+// instead of 4*K) and more warps fit per SM.
+template <int K, int P>
+MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
+                        const double* __restrict__ x, int len) {
+  const int nfull = len >> 2;
+  MC<K> s = zero<K>();
+#pragma unroll
+  for (int j0 = 0; j0 < 4; j0 += P) {
+    MC<K> L[P];
+#pragma unroll
+    for (int c = 0; c < P; ++c) L[c] = zero<K>();
+    for (int m = 0; m < nfull; ++m) {
+#pragma unroll
+      for (int c = 0; c < P; ++c) L[c] = add(L[c], sell_term<K>(vp, cp, st, x, 4 * m + j0 + c));
+    }
+#pragma unroll
+    for (int c = 0; c < P; ++c) s = add(s, L[c]);
+  }
+  for (int k = nfull * 4; k < len; ++k) s = add(s, sell_term<K>(vp, cp, st, x, k));
+  return s;
+}
+
+// Chunked row sum for latency-bound (DD) rows.  The row is consumed CH
+// elements at a time: first every column index of the chunk is loaded, then
+// every gather and matrix value, so a thread has CH independent loads in
+// flight per round trip instead of one; then the chunk's terms are added in
+// the reference order -- lanes on: element k goes to chain k % 4 over whole
+// 4-groups, chains combined (((0+L0)+L1)+L2)+L3, remainder serial; lanes off:
+// one chain.  Indices past the row end are clamped to its last element (a
+// valid address) and their terms discarded.
+#ifndef MPSG_DD_CHUNK
+#define MPSG_DD_CHUNK 0
+#endif
+template <int K, int ORDER, int CH>
+MPSG_DI MC<K> chunked_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
+                          const double* __restrict__ x, int len) {
+  constexpr bool LANES = ORDER != ORDER_SCALAR;
+  const int body = LANES ? (len & ~3) : len;  // elements summed into the chains
+  MC<K> L[LANES ? 4 : 1];
+#pragma unroll
+  for (int j = 0; j < (LANES ? 4 : 1); ++j) L[j] = zero<K>();
+  auto load_chunk = [&](int k0, int lim, MC<K>* p) {
+    int c[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) c[i] = __ldcs(cp + (int64_t)min(k0 + i, lim - 1) * 32);
+    MC<K> xv[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) xv[i] = load_aos<K>(x, c[i]);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) p[i] = mul(load_planes_stream<K>(vp, st, (int64_t)min(k0 + i, lim - 1) * 32), xv[i]);
+  };
+  MC<K> p[CH];
+  int k0 = 0;
+  if (len > 0) {
+    for (;;) {  // the last chunk holds the (1..3 element) remainder, if any
+      load_chunk(k0, len, p);
+#pragma unroll
+      for (int i = 0; i < CH; ++i)
+        if (k0 + i < body) L[LANES ? (i & 3) : 0] = add(L[LANES ? (i & 3) : 0], p[i]);
+      if (k0 + CH >= len) break;
+      k0 += CH;
+    }
+  }
+  MC<K> s;
+  if constexpr (LANES) {
+    s = zero<K>();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s = add(s, L[j]);
+#pragma unroll
+    for (int i = 0; i < CH; ++i)
+      if (k0 + i >= body && k0 + i < len) s = add(s, p[i]);
+  } else {
+    s = L[0];
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
 // SELL slice, real: one warp per slice of 32 rows, one thread per row.
 // ---------------------------------------------------------------------------
 template <int K, int ORDER>
-__global__ void __launch_bounds__(128) sell_real_kernel(SellView S, const double* __restrict__ x,
-                                                        double* __restrict__ y) {
+MPSG_DI void sell_real_body(const SellView& S, const double* __restrict__ x, double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= S.nslices) return;
@@ -60,50 +166,36 @@ __global__ void __launch_bounds__(128) sell_real_kernel(SellView S, const double
   const double* __restrict__ vp = S.val + base;
   const int64_t st = S.stride;
 
-  MC<K> acc = zero<K>();
-  if constexpr (ORDER == ORDER_SCALAR) {
+  MC<K> acc;
+  if constexpr (K == 2 && MPSG_DD_CHUNK > 0) {
+    acc = chunked_row<K, ORDER, MPSG_DD_CHUNK>(vp, cp, st, x, len);
+  } else if constexpr (ORDER == ORDER_SCALAR) {
+    acc = zero<K>();
     int k = 0;
     for (; k + 4 <= len; k += 4) {
       MC<K> p[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t e = (int64_t)(k + j) * 32;
-        MC<K> a = load_planes_stream<K>(vp, st, e);
-        MC<K> xv = load_aos<K>(x, __ldcs(cp + e));
-        p[j] = mul(a, xv);
-      }
+      for (int j = 0; j < 4; ++j) p[j] = sell_term<K>(vp, cp, st, x, k + j);
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc = add(acc, p[j]);
     }
-    for (; k < len; ++k) {
-      const int64_t e = (int64_t)k * 32;
-      MC<K> a = load_planes_stream<K>(vp, st, e);
-      MC<K> xv = load_aos<K>(x, __ldcs(cp + e));
-      acc = add(acc, mul(a, xv));
-    }
+    for (; k < len; ++k) acc = add(acc, sell_term<K>(vp, cp, st, x, k));
   } else {
-    MC<K> L[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) L[j] = zero<K>();
-    const int m4 = len & ~3;
-    for (int k = 0; k < m4; k += 4) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t e = (int64_t)(k + j) * 32;
-        MC<K> a = load_planes_stream<K>(vp, st, e);
-        MC<K> xv = load_aos<K>(x, __ldcs(cp + e));
-        L[j] = add(L[j], mul(a, xv));
-      }
-    }
-    acc = add(add(add(add(acc, L[0]), L[1]), L[2]), L[3]);
-    for (int k = m4; k < len; ++k) {
-      const int64_t e = (int64_t)k * 32;
-      MC<K> a = load_planes_stream<K>(vp, st, e);
-      MC<K> xv = load_aos<K>(x, __ldcs(cp + e));
-      acc = add(acc, mul(a, xv));
-    }
+    acc = lane4_row<K, MPSG_SELL_PAR(K)>(vp, cp, st, x, len);
   }
   if (row >= 0) store_aos<K>(y, row, acc);
+}
+
+template <int K, int ORDER>
+__global__ void MPSG_SELL_LB sell_real_kernel(SellView S, const double* __restrict__ x, double* __restrict__ y) {
+  sell_real_body<K, ORDER>(S, x, y);
+}
+// DD in the LANE4 order is memory-latency-bound: capped at 40 registers for
+// 12 resident blocks per SM (measured +17% on config 5, profiles/r01b_*).
+template <int K>
+__global__ void __launch_bounds__(128, 12) sell_real_lane4_lat_kernel(SellView S, const double* __restrict__ x,
+                                                                     double* __restrict__ y) {
+  sell_real_body<K, ORDER_LANE4>(S, x, y);
 }
 
 // ---------------------------------------------------------------------------
@@ -145,23 +237,23 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
       s2 = add(s2, p2);
     }
   } else {
-    MC<K> L1[4], L2[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) L1[j] = L2[j] = zero<K>();
-    const int m4 = len & ~3;
-    for (int k = 0; k < m4; k += 4) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t e = (int64_t)(k + j) * 16;
+    // the two sums' lane chains one at a time (reference order, fewer live
+    // accumulators), see lane4_row
+    const int nfull = len >> 2;
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      MC<K> L1 = zero<K>(), L2 = zero<K>();
+      for (int m = 0; m < nfull; ++m) {
+        const int64_t e = (int64_t)(4 * m + j) * 16;
         MC<K> a = load_planes_stream<K>(vp, st, e);
         const int c = __ldcs(cp + e);
-        L1[j] = add(L1[j], mul(a, load_aos<K>(x1, c)));
-        L2[j] = add(L2[j], mul(a, load_aos<K>(x2, c)));
+        L1 = add(L1, mul(a, load_aos<K>(x1, c)));
+        L2 = add(L2, mul(a, load_aos<K>(x2, c)));
       }
+      s1 = add(s1, L1);
+      s2 = add(s2, L2);
     }
-    s1 = add(add(add(add(s1, L1[0]), L1[1]), L1[2]), L1[3]);
-    s2 = add(add(add(add(s2, L2[0]), L2[1]), L2[2]), L2[3]);
-    for (int k = m4; k < len; ++k) {
+    for (int k = nfull * 4; k < len; ++k) {
       const int64_t e = (int64_t)k * 16;
       MC<K> a = load_planes_stream<K>(vp, st, e);
       const int c = __ldcs(cp + e);
@@ -277,22 +369,52 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
   const int64_t b = rb + (int64_t)(w - first) * L.chunk;
   const int64_t e = (b + L.chunk < re) ? b + L.chunk : re;
 
+  // U independent partial sums per lane (element k goes to partial
+  // ((k - b) / 32) % U), so U gathers are in flight per thread; combined in
+  // fixed order below.
+#ifndef MPSG_LONG_U
+#define MPSG_LONG_U 2
+#endif
+  constexpr int U = CPLX ? 1 : MPSG_LONG_U;
   MC<K> acc[NS];
+  MC<K> pu[U][NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) acc[s] = zero<K>();
-  for (int64_t k = b + lane; k < e; k += 32) {
-    const int c = __ldcs(L.col + k);
-    MC<K> are = load_planes_stream<K>(L.val, L.stride, k);
-    if constexpr (!CPLX) {
-      acc[0] = add(acc[0], mul(are, load_aos<K>(xre, c)));
-    } else {
-      MC<K> aim = load_planes_stream<K>(L.val + (int64_t)K * L.stride, L.stride, k);
-      MC<K> vr = load_aos<K>(xre, c), vi = load_aos<K>(xim, c);
-      acc[0] = add(acc[0], mul(are, vr));
-      acc[1] = add(acc[1], mul(aim, vi));
-      acc[2] = add(acc[2], mul(are, vi));
-      acc[3] = add(acc[3], mul(aim, vr));
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int s = 0; s < NS; ++s) pu[u][s] = zero<K>();
+  int64_t k = b + lane;
+  for (; k + 32 * (U - 1) < e; k += 32 * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t kk = k + 32 * u;
+      const int c = __ldcs(L.col + kk);
+      MC<K> are = load_planes_stream<K>(L.val, L.stride, kk);
+      if constexpr (!CPLX) {
+        pu[u][0] = add(pu[u][0], mul(are, load_aos<K>(xre, c)));
+      } else {
+        MC<K> aim = load_planes_stream<K>(L.val + (int64_t)K * L.stride, L.stride, kk);
+        MC<K> vr = load_aos<K>(xre, c), vi = load_aos<K>(xim, c);
+        pu[u][0] = add(pu[u][0], mul(are, vr));
+        pu[u][1] = add(pu[u][1], mul(aim, vi));
+        pu[u][2] = add(pu[u][2], mul(are, vi));
+        pu[u][3] = add(pu[u][3], mul(aim, vr));
+      }
     }
+  }
+#pragma unroll
+  for (int u = 0; u < U - 1; ++u) {  // remainder: at most U-1 more elements per lane
+    const int64_t kk = k + 32 * u;
+    if (kk < e) {
+      const int c = __ldcs(L.col + kk);
+      MC<K> are = load_planes_stream<K>(L.val, L.stride, kk);
+      pu[u][0] = add(pu[u][0], mul(are, load_aos<K>(xre, c)));
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    acc[s] = pu[0][s];
+#pragma unroll
+    for (int u = 1; u < U; ++u) acc[s] = add(acc[s], pu[u][s]);
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1)

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+S="cfg2:4:1 cfg2:3:1 cfg5:4:1 cfg4:2:2 cfg5:2:1 cfg1:2:1 cfg2:4:0 cfg2:3:0"
+python tools/kbench.py --tag par1 $S 2>&1 | grep -v Warn
+MPSG_LIB=$PWD/variants/par2.so python tools/kbench.py --tag par2 $S 2>&1 | grep -v Warn
+MPSG_LIB=$PWD/variants/par4.so python tools/kbench.py --tag par4 $S 2>&1 | grep -v Warn
+timeout 900 python -m pytest tests/test_gpu_spmv.py -x -q -m gpu 2>&1 | tail -3
