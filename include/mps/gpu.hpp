@@ -1,0 +1,332 @@
+// mps/gpu.hpp -- C++ drop-in for the reference's SpMV / CG path on B200.
+//
+// Header-only layer over the C ABI in mpsg.h (libmpsg.so).  It takes and
+// returns the reference's own types, so a caller of the reference
+// (/root/reference/proj/include/mps/) switches by changing the namespace:
+//
+//   reference (file:line)                                  drop-in here
+//   -----------------------------------------------------  -----------------------------------
+//   mps::spmv(const CsrMatrix<E>&, const std::vector<F>&,  mps::gpu::spmv (same signature)
+//             const KernelMode&)        kernels.hpp:348
+//   mps::spmv_complex(const ComplexSparseMatrix<E>&,       mps::gpu::spmv_complex (same)
+//             const ComplexVector<F>&, const KernelMode&)  kernels.hpp:399
+//   mps::CsrOperator<E> (Op concept)    krylov.hpp:101     mps::gpu::GpuCsrOperator<E>
+//   mps::solve_cg(op, b, cfg)           krylov.hpp:238     mps::gpu::solve_cg (device-resident)
+//                                                          -- or the reference solve_cg itself
+//                                                          with a GpuCsrOperator (same Op concept)
+//   mps::detail::partition_rows         kernels.hpp:63     mps::gpu::partition_rows
+//   mps::checksum                       bench.hpp:113      (unchanged; results are host vectors)
+//
+// Include the reference headers first (this file uses mps::CsrMatrix,
+// MultiComponent, KernelMode, SolverConfig, SolveResult, ...), then this one;
+// link libmpsg.so.  Semantics kept from the reference:
+//  * KernelMode::lanes_enabled selects the accumulation order, reproduced bit
+//    for bit (true: row_sum_lanes_pure, kernels.hpp:103; false:
+//    row_sum_scalar, kernels.hpp:90).  KernelMode::threads has no device
+//    meaning and is ignored.  The overloads taking mps::gpu::Order::Fast
+//    select the throughput order (componentwise error bound instead of bits).
+//  * dimension errors throw std::invalid_argument with the reference message
+//    (kernels.hpp:333-339); solver breakdown / divergence are reported in
+//    SolverReport, never thrown (krylov.hpp:46, 203-213).
+//  * host-vector calls are synchronous, like the reference.
+// Only the Pure matrix mode (matrix and vector in the same MultiComponent<K>,
+// K = 2, 3, 4) runs on the device; other element types fail to compile
+// (there is no CPU fallback).
+//
+// Matrices are uploaded once and cached by address (+ a structural
+// fingerprint).  A caller that rewrites a matrix's values in place between
+// calls must call mps::gpu::invalidate(A) (or hold an explicit DeviceCsr).
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "../mpsg.h"
+
+namespace mps {
+namespace gpu {
+
+namespace detail {
+template <class T>
+struct mc_width : std::integral_constant<int, 0> {};
+template <int K>
+struct mc_width<MultiComponent<K>> : std::integral_constant<int, K> {};
+
+inline void raise(mpsg_ctx* ctx, int rc) {
+  if (rc == MPSG_OK) return;
+  std::string msg = mpsg_last_error(ctx);
+  if (rc == MPSG_E_DIM) throw std::invalid_argument(msg);
+  throw std::runtime_error("mpsg error " + std::to_string(rc) + ": " + msg);
+}
+}  // namespace detail
+
+// ---------------------------------------------------------------- context
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    int rc = mpsg_ctx_create(device, &ctx_);
+    if (rc != MPSG_OK) throw std::runtime_error("mpsg_ctx_create failed: no usable sm_100a GPU");
+  }
+  ~Context() { mpsg_ctx_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  mpsg_ctx* get() const { return ctx_; }
+  void check(int rc) const { detail::raise(ctx_, rc); }
+
+  // Process-wide default context on device 0 (like the reference's implicit
+  // host execution); one host thread at a time, like mpsg_ctx.
+  static Context& instance() {
+    static Context c(0);
+    return c;
+  }
+
+ private:
+  mpsg_ctx* ctx_ = nullptr;
+};
+
+// Accumulation order.  Lane4 / Scalar are the reference's lanes-on /
+// lanes-off orders (bit-exact); Fast reorders long rows for throughput and
+// is checked against |y - y_ref| <= 4 * rowlen * u * sum|a||x|.
+enum class Order : int { Scalar = MPSG_ORDER_SCALAR, Lane4 = MPSG_ORDER_LANE4, Fast = MPSG_ORDER_FAST };
+inline Order order_of(const KernelMode& m) { return m.lanes_enabled ? Order::Lane4 : Order::Scalar; }
+
+// ------------------------------------------------------------- matrices
+// Device copy of a CsrMatrix<MultiComponent<K>> or of a
+// ComplexSparseMatrix<MultiComponent<K>> (one shared structure).
+template <class E>
+class DeviceCsr {
+  static constexpr int K = detail::mc_width<E>::value;
+  static_assert(K >= 2, "mps::gpu: device matrices hold MultiComponent<2|3|4> values (Pure mode)");
+
+ public:
+  DeviceCsr(const CsrMatrix<E>& A, Context& ctx = Context::instance()) : ctx_(&ctx) {
+    const double* planes[K];
+    for (int j = 0; j < K; ++j) planes[j] = A.values.component(j);
+    ctx.check(mpsg_csr_upload(ctx.get(), K, 0, A.nrows, A.ncols, A.indptr.data(), A.indices.data(), planes,
+                              &h_));
+    nrows_ = A.nrows;
+    ncols_ = A.ncols;
+  }
+  DeviceCsr(const ComplexSparseMatrix<E>& A, Context& ctx = Context::instance()) : ctx_(&ctx) {
+    check_split_structure(A);  // sparse.hpp:254-259
+    const double* planes[2 * K];
+    for (int j = 0; j < K; ++j) {
+      planes[j] = A.re.values.component(j);
+      planes[K + j] = A.im.values.component(j);
+    }
+    ctx.check(mpsg_csr_upload(ctx.get(), K, 1, A.re.nrows, A.re.ncols, A.re.indptr.data(), A.re.indices.data(),
+                              planes, &h_));
+    nrows_ = A.re.nrows;
+    ncols_ = A.re.ncols;
+  }
+  ~DeviceCsr() { mpsg_csr_destroy(h_); }
+  DeviceCsr(const DeviceCsr&) = delete;
+  DeviceCsr& operator=(const DeviceCsr&) = delete;
+
+  std::int64_t rows() const { return nrows_; }
+  std::int64_t cols() const { return ncols_; }
+  const mpsg_csr* get() const { return h_; }
+  Context& context() const { return *ctx_; }
+
+ private:
+  Context* ctx_;
+  mpsg_csr* h_ = nullptr;
+  std::int64_t nrows_ = 0, ncols_ = 0;
+};
+
+template <class E>
+std::vector<E> spmv(const DeviceCsr<E>& A, const std::vector<E>& v, Order order) {
+  std::vector<E> y(static_cast<std::size_t>(A.rows()));
+  static_assert(sizeof(E) == sizeof(double) * detail::mc_width<E>::value, "MultiComponent must be K doubles");
+  A.context().check(mpsg_spmv(A.context().get(), A.get(), static_cast<int>(order), static_cast<std::int64_t>(v.size()),
+                              reinterpret_cast<const double*>(v.data()), reinterpret_cast<double*>(y.data())));
+  return y;
+}
+
+template <class E>
+std::vector<E> spmv(const DeviceCsr<E>& A, const std::vector<E>& v, const KernelMode& mode) {
+  return spmv(A, v, order_of(mode));
+}
+
+template <class E>
+ComplexVector<E> spmv_complex(const DeviceCsr<E>& A, const ComplexVector<E>& v, Order order) {
+  if (v.re.size() != v.im.size()) throw std::invalid_argument("spmv_complex: re/im vector length mismatch");
+  ComplexVector<E> y;
+  y.re.resize(static_cast<std::size_t>(A.rows()));
+  y.im.resize(static_cast<std::size_t>(A.rows()));
+  A.context().check(mpsg_spmv_complex(A.context().get(), A.get(), static_cast<int>(order),
+                                      static_cast<std::int64_t>(v.re.size()),
+                                      reinterpret_cast<const double*>(v.re.data()),
+                                      reinterpret_cast<const double*>(v.im.data()),
+                                      reinterpret_cast<double*>(y.re.data()),
+                                      reinterpret_cast<double*>(y.im.data())));
+  return y;
+}
+
+template <class E>
+ComplexVector<E> spmv_complex(const DeviceCsr<E>& A, const ComplexVector<E>& v, const KernelMode& mode) {
+  return spmv_complex(A, v, order_of(mode));
+}
+
+// --------------------------------------------------- upload cache (drop-in)
+namespace detail {
+struct CacheKey {
+  const void* addr;
+  const void* indptr;
+  const void* plane0;
+  std::int64_t nnz;
+  bool operator<(const CacheKey& o) const {
+    return std::tie(addr, indptr, plane0, nnz) < std::tie(o.addr, o.indptr, o.plane0, o.nnz);
+  }
+};
+template <class E>
+std::map<CacheKey, std::shared_ptr<DeviceCsr<E>>>& cache() {
+  static std::map<CacheKey, std::shared_ptr<DeviceCsr<E>>> c;
+  return c;
+}
+template <class E>
+CacheKey key_of(const CsrMatrix<E>& A) {
+  return {&A, A.indptr.data(), A.values.component(0), A.nnz()};
+}
+template <class E>
+CacheKey key_of(const ComplexSparseMatrix<E>& A) {
+  return {&A, A.re.indptr.data(), A.re.values.component(0), A.re.nnz()};
+}
+template <class E, class M>
+const DeviceCsr<E>& cached(const M& A) {
+  auto& c = cache<E>();
+  const CacheKey k = key_of(A);
+  auto it = c.find(k);
+  if (it == c.end()) {
+    // drop stale entries for the same address (the matrix was rebuilt)
+    for (auto jt = c.begin(); jt != c.end();) jt = (jt->first.addr == k.addr) ? c.erase(jt) : std::next(jt);
+    it = c.emplace(k, std::make_shared<DeviceCsr<E>>(A)).first;
+  }
+  return *it->second;
+}
+}  // namespace detail
+
+template <class E>
+void invalidate(const CsrMatrix<E>& A) {
+  auto& c = detail::cache<E>();
+  for (auto it = c.begin(); it != c.end();) it = (it->first.addr == &A) ? c.erase(it) : std::next(it);
+}
+template <class E>
+void invalidate(const ComplexSparseMatrix<E>& A) {
+  auto& c = detail::cache<E>();
+  for (auto it = c.begin(); it != c.end();) it = (it->first.addr == &A) ? c.erase(it) : std::next(it);
+}
+
+// ---------------------------------------- reference-signature drop-ins
+// mps::spmv (kernels.hpp:348-366)
+template <class E, class F>
+std::vector<F> spmv(const CsrMatrix<E>& A, const std::vector<F>& v, const KernelMode& mode) {
+  static_assert(std::is_same<E, F>::value, "mps::gpu::spmv: only the Pure mode (E == F) runs on the device");
+  if (static_cast<std::size_t>(A.ncols) != v.size())  // kernels.hpp:333-339
+    throw std::invalid_argument("spmv: vector length " + std::to_string(v.size()) +
+                                " does not match matrix dimension " + std::to_string(A.ncols));
+  return spmv(detail::cached<E>(A), v, mode);
+}
+
+// mps::spmv_complex (kernels.hpp:399-416)
+template <class E, class F>
+ComplexVector<F> spmv_complex(const ComplexSparseMatrix<E>& A, const ComplexVector<F>& v, const KernelMode& mode) {
+  static_assert(std::is_same<E, F>::value, "mps::gpu::spmv_complex: only the Pure mode runs on the device");
+  if (v.re.size() != v.im.size()) throw std::invalid_argument("spmv_complex: re/im vector length mismatch");
+  if (static_cast<std::size_t>(A.re.ncols) != v.re.size())
+    throw std::invalid_argument("spmv: vector length " + std::to_string(v.re.size()) +
+                                " does not match matrix dimension " + std::to_string(A.re.ncols));
+  return spmv_complex(detail::cached<E>(A), v, mode);
+}
+
+// nnz-balanced contiguous row bounds (kernels.hpp:63-80)
+inline std::vector<std::int64_t> partition_rows(const std::vector<std::int64_t>& indptr, std::int64_t nrows,
+                                                int parts) {
+  std::vector<std::int64_t> b(static_cast<std::size_t>(parts) + 1);
+  if (mpsg_partition_rows(indptr.data(), nrows, parts, b.data()) != MPSG_OK)
+    throw std::invalid_argument("partition_rows: bad arguments");
+  return b;
+}
+
+// ------------------------------------------------------------- solvers
+// The Op concept of krylov.hpp:101-120 over a device-resident matrix: the
+// reference's own solve_cg / solve_bicg / ... run unchanged with it, every
+// apply() being one device SpMV.
+template <class MatE>
+struct GpuCsrOperator {
+  const DeviceCsr<MatE>* matrix = nullptr;
+  int threads = 1;  // ignored on the device (kept for the reference's shape)
+  bool lanes_enabled = true;
+  bool fast = false;
+
+  std::int64_t rows() const { return matrix->rows(); }
+  std::int64_t cols() const { return matrix->cols(); }
+  KernelMode mode() const { return KernelMode{{}, MatrixMode::Pure, false, threads, lanes_enabled}; }
+  Order order() const { return fast ? Order::Fast : order_of(mode()); }
+  template <class F>
+  std::vector<F> apply(const std::vector<F>& x) const {
+    return gpu::spmv(*matrix, x, order());
+  }
+  template <class F>
+  std::vector<F> apply_transposed(const std::vector<F>&) const {
+    throw std::logic_error("mps::gpu::GpuCsrOperator: the transposed product is not on the device yet");
+  }
+};
+
+// Device-resident CG (krylov.hpp:238-281): vectors and scalars never leave
+// the GPU; the residual history, status and true residual come back in the
+// reference's SolverReport.  Only rel_tol, abs_tol, max_iters, x0 and
+// lanes_enabled of SolverConfig are read (as by the reference CG).
+template <class E>
+SolveResult<E> solve_cg(const GpuCsrOperator<E>& op, const std::vector<E>& b, const SolverConfig& cfg) {
+  constexpr int K = detail::mc_width<E>::value;
+  cfg.validate();  // krylov.hpp:69-75
+  if (op.rows() != op.cols())
+    throw std::invalid_argument("solver: operator must be square, got " + std::to_string(op.rows()) + "x" +
+                                std::to_string(op.cols()));
+  if (static_cast<std::size_t>(op.cols()) != b.size())
+    throw std::invalid_argument("solver: rhs length does not match the operator");
+  std::vector<E> x0;
+  if (!cfg.x0.empty()) {
+    if (cfg.x0.size() != b.size()) throw std::invalid_argument("solver: x0 length does not match the rhs");
+    x0.resize(b.size());
+    for (std::size_t i = 0; i < b.size(); ++i) x0[i] = E(cfg.x0[i]);  // scalar_like (krylov.hpp:178)
+  }
+  mpsg_cg_config c{cfg.rel_tol, cfg.abs_tol, cfg.max_iters, 32, 1};
+  mpsg_cg_report rep{};
+  SolveResult<E> res;
+  res.x.resize(b.size());
+  std::vector<double> hist(static_cast<std::size_t>(cfg.max_iters) + 1);
+  const int order = op.fast ? MPSG_ORDER_FAST
+                            : (cfg.lanes_enabled && op.lanes_enabled ? MPSG_ORDER_LANE4 : MPSG_ORDER_SCALAR);
+  Context& ctx = op.matrix->context();
+  ctx.check(mpsg_cg(ctx.get(), op.matrix->get(), order, static_cast<std::int64_t>(b.size()),
+                    reinterpret_cast<const double*>(b.data()),
+                    x0.empty() ? nullptr : reinterpret_cast<const double*>(x0.data()), &c,
+                    reinterpret_cast<double*>(res.x.data()), hist.data(), static_cast<std::int64_t>(hist.size()),
+                    &rep));
+  static_assert(K >= 2, "device CG runs on MultiComponent<K>");
+  auto& r = res.report;
+  r.status = static_cast<SolverStatus>(rep.status);
+  r.converged = rep.converged != 0;
+  r.detail = rep.detail;
+  r.iterations = rep.iterations;
+  r.residual_history.assign(hist.begin(), hist.begin() + rep.history_len);
+  r.rhs_norm = rep.rhs_norm;
+  r.final_recurrence_residual = rep.final_recurrence_residual;
+  r.final_true_residual = rep.final_true_residual;
+  r.setup_seconds = rep.setup_seconds;
+  r.solve_seconds = rep.solve_seconds;
+  return res;
+}
+
+}  // namespace gpu
+}  // namespace mps
