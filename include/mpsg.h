@@ -165,6 +165,45 @@ MPSG_API int mpsg_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, 
             const double* x0, const mpsg_cg_config* cfg, double* x_out, double* history,
             int64_t history_cap, mpsg_cg_report* report);
 
+/* ---- row-sharded multi-GPU (one process per GPU, NCCL) ------------------ */
+/* Rank r owns rows [bounds[r], bounds[r+1]) (mpsg_partition_rows gives the
+ * reference's equal-nnz rule, kernels.hpp:63-80) and the same block of x and
+ * y; per SpMV only the x halo moves (ncclSend/ncclRecv, NVLink/NVSwitch); CG
+ * dot products are allgathered per-rank partials summed in rank order.  The
+ * exact orders stay bit-exact for any partition. */
+typedef struct mpsg_comm mpsg_comm;
+typedef struct mpsg_dcsr mpsg_dcsr;
+/* NCCL unique id (128 bytes) created on one rank and broadcast by the caller. */
+MPSG_API int mpsg_comm_unique_id(unsigned char* id);
+/* id may be NULL when nranks == 1.  NCCL is loaded at run time (libnccl.so.2). */
+MPSG_API int mpsg_comm_create(mpsg_ctx* ctx, int nranks, int rank, const unsigned char* id, mpsg_comm** out);
+MPSG_API void mpsg_comm_destroy(mpsg_comm* comm);
+/* This rank's rows [row_begin, row_end) of a square nglobal x nglobal matrix:
+ * indptr rebased (row_end-row_begin+1 entries), global column indices, K or
+ * 2K planes.  Collective: builds the halo plan with every rank. */
+MPSG_API int mpsg_dcsr_upload(mpsg_comm* comm, int K, int is_complex, int64_t nglobal, int64_t row_begin,
+                              int64_t row_end, const int64_t* indptr, const int64_t* indices,
+                              const double* const* planes, mpsg_dcsr** out);
+MPSG_API void mpsg_dcsr_destroy(mpsg_dcsr* A);
+/* bounds: nranks+1 entries (may be NULL); halo_rows: rows received per SpMV. */
+MPSG_API int mpsg_dcsr_info(const mpsg_dcsr* A, int64_t* bounds, int64_t* halo_rows);
+/* y_local = (A x)[row block]; x_local / y_local are this rank's blocks.
+ * Collective (every rank calls it with the same order). */
+MPSG_API int mpsg_dspmv(mpsg_dcsr* A, int order, const double* x_local, double* y_local);
+MPSG_API int mpsg_dspmv_dev(mpsg_dcsr* A, int order, const double* d_x_local, double* d_y_local, void* stream);
+MPSG_API int mpsg_dspmv_complex_dev(mpsg_dcsr* A, int order, const double* d_xr_local, const double* d_xi_local,
+                                   double* d_yr_local, double* d_yi_local, void* stream);
+/* Row-sharded CG (krylov.hpp:238-281); b / x0 / x_out are this rank's blocks,
+ * the history and report are identical on every rank.  Collective. */
+MPSG_API int mpsg_dcg(mpsg_dcsr* A, int order, const double* b_local, const double* x0_local,
+                      const mpsg_cg_config* cfg, double* x_out_local, double* history, int64_t history_cap,
+                      mpsg_cg_report* report);
+/* Host-only halo plan: for every peer q, the interval of my rows q reads
+ * (send[2q], send[2q+1]) and of q's rows I read (recv[...]); need[2q..] is
+ * the column interval rank q reads.  Empty intervals are (0, 0). */
+MPSG_API int mpsg_halo_plan(int nranks, int rank, const int64_t* bounds, const int64_t* need, int64_t* send,
+                            int64_t* recv);
+
 /* ---- host utilities ---------------------------------------------------- */
 /* nnz-balanced contiguous row bounds (kernels.hpp:63-80), parts+1 entries. */
 MPSG_API int mpsg_partition_rows(const int64_t* indptr, int64_t nrows, int parts, int64_t* bounds);

@@ -76,7 +76,10 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_ctx_set_layout", "mpsg_ctx_synchronize", "mpsg_csr_upload", "mpsg_csr_destroy",
            "mpsg_csr_get_stats", "mpsg_spmv", "mpsg_spmv_dev", "mpsg_spmv_complex",
            "mpsg_spmv_complex_dev", "mpsg_cg", "mpsg_partition_rows", "mpsg_checksum",
-           "mpsg_checksum_complex", "mpsg_version", "mpsg_measure_fp64_peak", "mpsg_mc_op_dev")
+           "mpsg_checksum_complex", "mpsg_version", "mpsg_measure_fp64_peak", "mpsg_mc_op_dev",
+           "mpsg_comm_unique_id", "mpsg_comm_create", "mpsg_comm_destroy", "mpsg_dcsr_upload",
+           "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
+           "mpsg_dcg", "mpsg_halo_plan")
 
 
 def lib():
@@ -113,6 +116,19 @@ def lib():
     L.mpsg_version.restype = ctypes.c_char_p
     L.mpsg_measure_fp64_peak.argtypes = [_P, ctypes.POINTER(_f64)]
     L.mpsg_mc_op_dev.argtypes = [_P, _i32, _i32, _i64, _P, _P, _P]
+    L.mpsg_comm_unique_id.argtypes = [_P]
+    L.mpsg_comm_create.argtypes = [_P, _i32, _i32, _P, ctypes.POINTER(_P)]
+    L.mpsg_comm_destroy.argtypes = [_P]
+    L.mpsg_dcsr_upload.argtypes = [_P, _i32, _i32, _i64, _i64, _i64, _P, _P, ctypes.POINTER(_P),
+                                   ctypes.POINTER(_P)]
+    L.mpsg_dcsr_destroy.argtypes = [_P]
+    L.mpsg_dcsr_info.argtypes = [_P, _P, _P]
+    L.mpsg_dspmv.argtypes = [_P, _i32, _P, _P]
+    L.mpsg_dspmv_dev.argtypes = [_P, _i32, _P, _P, _P]
+    L.mpsg_dspmv_complex_dev.argtypes = [_P, _i32, _P, _P, _P, _P, _P]
+    L.mpsg_dcg.argtypes = [_P, _i32, _P, _P, ctypes.POINTER(_CgConfig), _P, _P, _i64,
+                           ctypes.POINTER(_CgReport)]
+    L.mpsg_halo_plan.argtypes = [_i32, _i32, _P, _P, _P, _P]
     _lib = L
     return L
 
@@ -381,6 +397,166 @@ def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult
         final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
         solve_seconds=rep.solve_seconds)
     return SolveResult(x, report)
+
+
+# --------------------------------------------------------------------------- multi-GPU
+NCCL_ID_BYTES = 128
+
+
+class Comm:
+    """One rank of a row-sharded group (mpsg_comm over NCCL).  ``unique_id``
+    comes from ``Comm.unique_id()`` on one rank, broadcast by the caller (e.g.
+    torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, ctx: Context, nranks: int = 1, rank: int = 0, unique_id: bytes | None = None):
+        self.ctx, self.nranks, self.rank = ctx, nranks, rank
+        buf = None
+        if unique_id is not None:
+            buf = ctypes.create_string_buffer(bytes(unique_id), NCCL_ID_BYTES)
+        h = _P()
+        ctx.check(lib().mpsg_comm_create(ctx.h, nranks, rank, buf, ctypes.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+        rc = lib().mpsg_comm_unique_id(buf)
+        if rc != E_OK:
+            raise MpsgError(rc, "mpsg_comm_unique_id failed (libnccl.so.2 not loadable?)")
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mpsg_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard_rows(A, row_begin: int, row_end: int):
+    """Rows [row_begin, row_end) of a reference-layout CSR, indptr rebased,
+    global column indices kept (host helper for DistCsr)."""
+    from types import SimpleNamespace
+
+    ip = np.asarray(A.indptr, dtype=np.int64)
+    lo, hi = int(ip[row_begin]), int(ip[row_end])
+    return SimpleNamespace(nrows=row_end - row_begin, ncols=int(A.ncols), indptr=ip[row_begin:row_end + 1] - lo,
+                           indices=np.asarray(A.indices, dtype=np.int64)[lo:hi],
+                           planes=np.asarray(A.planes)[:, lo:hi])
+
+
+class DistCsr:
+    """This rank's row block of a square matrix (mpsg_dcsr).  Collective."""
+
+    def __init__(self, comm: Comm, A_local, K: int, nglobal: int, row_begin: int, row_end: int,
+                 is_complex: bool = False):
+        self.comm, self.K, self.is_complex = comm, K, bool(is_complex)
+        self.nglobal, self.row_begin, self.row_end = int(nglobal), int(row_begin), int(row_end)
+        indptr = np.ascontiguousarray(A_local.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(A_local.indices, dtype=np.int64)
+        nplanes = 2 * K if is_complex else K
+        plist = [np.ascontiguousarray(np.asarray(A_local.planes)[j], dtype=np.float64) for j in range(nplanes)]
+        parr = (_P * nplanes)(*[p.ctypes.data for p in plist])
+        h = _P()
+        comm.ctx.check(lib().mpsg_dcsr_upload(comm.h, K, 1 if is_complex else 0, self.nglobal, self.row_begin,
+                                              self.row_end, _p(indptr), _p(indices), parr, ctypes.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_global(cls, comm: Comm, A, K: int, is_complex: bool = False, bounds=None):
+        """Shard a full host matrix by the reference's equal-nnz rule (or ``bounds``)."""
+        if bounds is None:
+            bounds = partition_rows(A.indptr, int(A.nrows), comm.nranks)
+        b, e = int(bounds[comm.rank]), int(bounds[comm.rank + 1])
+        return cls(comm, shard_rows(A, b, e), K, int(A.nrows), b, e, is_complex)
+
+    def info(self):
+        b = np.empty(self.comm.nranks + 1, dtype=np.int64)
+        halo = _i64()
+        self.comm.ctx.check(lib().mpsg_dcsr_info(self.h, _p(b), ctypes.byref(halo)))
+        return b, int(halo.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mpsg_dcsr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dspmv(A: DistCsr, x_local, mode: KernelMode | int | None = None) -> np.ndarray:
+    """y_local = (A x)[this rank's rows]; x_local is this rank's block.  Collective."""
+    x = _aos(x_local, "spmv")
+    if x.shape[0] != A.row_end - A.row_begin or x.shape[1] != A.K:
+        raise ValueError(f"spmv: vector length {x.shape[0]} does not match the row block "
+                         f"{A.row_end - A.row_begin}")
+    y = np.empty((A.row_end - A.row_begin, A.K))
+    A.comm.ctx.check(lib().mpsg_dspmv(A.h, _order(mode), _p(x), _p(y)))
+    return y
+
+
+def dspmv_dev(A: DistCsr, d_x: int, d_y: int, order: int = ORDER_LANE4, stream: int | None = None):
+    A.comm.ctx.check(lib().mpsg_dspmv_dev(A.h, order, d_x, d_y, stream))
+
+
+def dspmv_complex_dev(A: DistCsr, d_xr: int, d_xi: int, d_yr: int, d_yi: int, order: int = ORDER_LANE4,
+                      stream: int | None = None):
+    A.comm.ctx.check(lib().mpsg_dspmv_complex_dev(A.h, order, d_xr, d_xi, d_yr, d_yi, stream))
+
+
+def dsolve_cg(A: DistCsr, b_local, cfg: SolverConfig | None = None) -> SolveResult:
+    """Row-sharded device CG; b_local / result x are this rank's blocks.  Collective."""
+    cfg = cfg or SolverConfig()
+    cfg.validate()
+    bb = _aos(b_local, "solver")
+    if bb.shape[0] != A.row_end - A.row_begin:
+        raise ValueError("solver: rhs length does not match the operator")
+    x0 = None
+    if cfg.x0 is not None and len(cfg.x0) > 0:
+        x0 = np.zeros_like(bb)
+        x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)[A.row_begin:A.row_end]
+    c = _CgConfig(cfg.rel_tol, cfg.abs_tol, cfg.max_iters, cfg.check_every, 1 if cfg.use_graph else 0)
+    rep = _CgReport()
+    x = np.empty_like(bb)
+    hist = np.empty(cfg.max_iters + 1)
+    order = ORDER_FAST if cfg.fast else (ORDER_LANE4 if cfg.lanes_enabled else ORDER_SCALAR)
+    A.comm.ctx.check(lib().mpsg_dcg(A.h, order, _p(bb), _p(x0), ctypes.byref(c), _p(x), _p(hist), len(hist),
+                                    ctypes.byref(rep)))
+    report = SolverReport(
+        status=SolverStatus(rep.status), converged=bool(rep.converged), detail=rep.detail.decode(),
+        iterations=int(rep.iterations), residual_history=hist[: rep.history_len].tolist(),
+        rhs_norm=rep.rhs_norm, final_recurrence_residual=rep.final_recurrence_residual,
+        final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
+        solve_seconds=rep.solve_seconds)
+    return SolveResult(x, report)
+
+
+def halo_plan(nranks: int, rank: int, bounds, need):
+    """Host-only halo plan (mpsg_halo_plan): returns (send, recv), each [nranks, 2]."""
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    nd = np.ascontiguousarray(need, dtype=np.int64).reshape(-1)
+    send = np.empty(2 * nranks, dtype=np.int64)
+    recv = np.empty(2 * nranks, dtype=np.int64)
+    rc = lib().mpsg_halo_plan(nranks, rank, _p(b), _p(nd), _p(send), _p(recv))
+    if rc != E_OK:
+        raise ValueError("halo_plan: bad arguments")
+    return send.reshape(nranks, 2), recv.reshape(nranks, 2)
+
+
+def need_interval(A_local, row_begin: int, row_end: int):
+    """Column interval a row block reads (its own block included)."""
+    idx = np.asarray(A_local.indices)
+    lo = min(row_begin, int(idx.min())) if len(idx) else row_begin
+    hi = max(row_end, int(idx.max()) + 1) if len(idx) else row_end
+    return lo, hi
 
 
 # --------------------------------------------------------------------------- host utilities

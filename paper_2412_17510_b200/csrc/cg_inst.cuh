@@ -1,10 +1,18 @@
 // cg_inst.cuh -- device CG driver template, instantiated per K by cg_k{2,3,4}.cu.
+//
+// One driver for both the single-GPU solve (mpsg_cg) and the row-sharded
+// multi-GPU solve (mpsg_dcg): with a distributed matrix D, vectors are this
+// rank's row block, p lives in a global-length buffer whose halo is exchanged
+// before every SpMV, and every dot product is reduced per rank, allgathered
+// and summed in rank order (dist.h).  Without D the reductions finish in the
+// last block of the reduction kernel itself.
 #pragma once
 #include <algorithm>
 #include <chrono>
 #include <cstring>
 
 #include "cg_kernels.cuh"
+#include "dist.h"
 #include "internal.h"
 
 namespace mpsg {
@@ -14,73 +22,121 @@ inline double now_s() {
 }
 
 template <int K>
-int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, const double* x0,
-           const mpsg_cg_config* cfg, double* x_out, double* history, int64_t history_cap,
-           mpsg_cg_report* rep) {
+int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, const double* b_host,
+              const double* x0, const mpsg_cg_config* cfg, double* x_out, double* history, int64_t history_cap,
+              mpsg_cg_report* rep) {
   const double t0 = now_s();
-  const int64_t n = A->nrows;
+  const int64_t n = A->nrows;  // local rows
+  const int64_t nx = D ? D->nglobal : n;
+  const int64_t off = D ? D->row_begin : 0;
+  const int P = D ? D->comm->nranks : 1;
   const size_t vb = (size_t)n * K * sizeof(double);
   cudaStream_t st = ctx->stream;
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(DOT_MAX_BLOCKS, (n + 2047) / 2048));
-  double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *part = nullptr,
-         *hist = nullptr;
+  double *b = nullptr, *x = nullptr, *r = nullptr, *pfull = nullptr, *q = nullptr, *part = nullptr,
+         *hist = nullptr, *loc = nullptr, *gath = nullptr;
   CgState<K>* dst = nullptr;
   const int64_t max_iters = cfg->max_iters;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t graph = nullptr;
   auto cleanup = [&]() {
-    void* ps[] = {b, x, r, p, q, part, hist, dst};
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    void* ps[] = {b, x, r, pfull, q, part, hist, loc, gath, dst};
     for (void* v : ps)
       if (v) cudaFree(v);
   };
   int rc = MPSG_OK;
-#define CG_TRY(call)                                                                         \
-  do {                                                                                       \
-    cudaError_t e_ = (call);                                                                 \
-    if (e_ != cudaSuccess) {                                                                 \
-      rc = fail(ctx, e_ == cudaErrorMemoryAllocation ? MPSG_E_OOM : MPSG_E_CUDA, "cg: %s: %s", #call, \
-                cudaGetErrorString(e_));                                                     \
-      cleanup();                                                                             \
-      return rc;                                                                             \
-    }                                                                                        \
+#define CG_TRY(call)                                                                                    \
+  do {                                                                                                  \
+    cudaError_t e_ = (call);                                                                            \
+    if (e_ != cudaSuccess) {                                                                            \
+      rc = fail(ctx, e_ == cudaErrorMemoryAllocation ? MPSG_E_OOM : MPSG_E_CUDA, "cg: %s: %s", #call,   \
+                cudaGetErrorString(e_));                                                                \
+      cleanup();                                                                                        \
+      return rc;                                                                                        \
+    }                                                                                                   \
   } while (0)
-  CG_TRY(cudaMalloc(&b, vb));
-  CG_TRY(cudaMalloc(&x, vb));
-  CG_TRY(cudaMalloc(&r, vb));
-  CG_TRY(cudaMalloc(&p, vb));
-  CG_TRY(cudaMalloc(&q, vb));
+#define CG_RC(expr)     \
+  do {                  \
+    rc = (expr);        \
+    if (rc != MPSG_OK) { \
+      cleanup();        \
+      return rc;        \
+    }                   \
+  } while (0)
+  CG_TRY(cudaMalloc(&b, vb ? vb : 8));
+  CG_TRY(cudaMalloc(&x, vb ? vb : 8));
+  CG_TRY(cudaMalloc(&r, vb ? vb : 8));
+  CG_TRY(cudaMalloc(&pfull, (size_t)std::max<int64_t>(nx, 1) * K * sizeof(double)));
+  CG_TRY(cudaMalloc(&q, vb ? vb : 8));
   CG_TRY(cudaMalloc(&part, (size_t)G * K * sizeof(double)));
   CG_TRY(cudaMalloc(&hist, (size_t)(max_iters + 1) * sizeof(double)));
   CG_TRY(cudaMalloc(&dst, sizeof(CgState<K>)));
-  CG_TRY(cudaMemcpyAsync(b, b_host, vb, cudaMemcpyHostToDevice, st));
+  if (D) {
+    CG_TRY(cudaMalloc(&loc, (size_t)K * sizeof(double)));
+    CG_TRY(cudaMalloc(&gath, (size_t)P * K * sizeof(double)));
+  }
+  double* p = pfull + off * K;  // this rank's block of p
+
+  // one reduction: fused scalar step (single GPU) or partial -> allgather ->
+  // rank-ordered sum -> scalar step (multi-GPU)
+  auto reduce = [&](auto mode_tag, int post, const double* u, const double* v, double* xx, double* rr,
+                    int gate) -> int {
+    constexpr int MODE = decltype(mode_tag)::value;
+    cg_reduce_kernel<K, MODE><<<G, DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part, gate, D ? loc : nullptr);
+    if (D) {
+      int e = allgather_mc(D->comm, loc, gath, K, st);
+      if (e) return e;
+      cg_post_gathered_kernel<K><<<1, 1, 0, st>>>(dst, post, gath, P, gate);
+    }
+    return cudaGetLastError() == cudaSuccess ? MPSG_OK : fail(ctx, MPSG_E_CUDA, "cg: reduction launch failed");
+  };
+  using Dot = std::integral_constant<int, 0>;
+  using Upd = std::integral_constant<int, 1>;
+  using Res = std::integral_constant<int, 2>;
+  // q = A p over the global-length p (halo first when sharded)
+  auto apply = [&](double* out) -> int {
+    if (D) {
+      int e = halo_exchange(D, pfull, st);
+      if (e) return e;
+    }
+    return launch_spmv(ctx, A, order, pfull, nullptr, out, nullptr, st);
+  };
+
+  if (vb) CG_TRY(cudaMemcpyAsync(b, b_host, vb, cudaMemcpyHostToDevice, st));
   cg_init_state_kernel<K><<<1, 1, 0, st>>>(dst, cfg->rel_tol, cfg->abs_tol, (long long)max_iters, hist);
   // bnorm = norm2(b) (krylov.hpp:185)
-  cg_reduce_kernel<K, 0><<<G, DOT_THREADS, 0, st>>>(dst, POST_BNORM, n, b, b, nullptr, nullptr, part, 0);
+  CG_RC(reduce(Dot{}, POST_BNORM, b, b, nullptr, nullptr, 0));
   if (x0) {
     // x = x0; r = b - A x0 (krylov.hpp:174-181)
-    CG_TRY(cudaMemcpyAsync(x, x0, vb, cudaMemcpyHostToDevice, st));
-    if ((rc = launch_spmv(ctx, A, order, x, nullptr, r, nullptr, st)) != MPSG_OK) {
-      cleanup();
-      return rc;
+    if (vb) {
+      CG_TRY(cudaMemcpyAsync(x, x0, vb, cudaMemcpyHostToDevice, st));
+      CG_TRY(cudaMemcpyAsync(p, x, vb, cudaMemcpyDeviceToDevice, st));
     }
-    cg_reduce_kernel<K, 2><<<G, DOT_THREADS, 0, st>>>(dst, POST_R0, n, b, nullptr, r, nullptr, part, 0);
+    CG_RC(apply(r));
+    CG_RC(reduce(Res{}, POST_R0, b, nullptr, r, nullptr, 0));
   } else {
-    CG_TRY(cudaMemsetAsync(x, 0, vb, st));
-    CG_TRY(cudaMemcpyAsync(r, b, vb, cudaMemcpyDeviceToDevice, st));
-    cg_reduce_kernel<K, 0><<<G, DOT_THREADS, 0, st>>>(dst, POST_R0, n, r, r, nullptr, nullptr, part, 0);
+    if (vb) {
+      CG_TRY(cudaMemsetAsync(x, 0, vb, st));
+      CG_TRY(cudaMemcpyAsync(r, b, vb, cudaMemcpyDeviceToDevice, st));
+    }
+    CG_RC(reduce(Dot{}, POST_R0, r, r, nullptr, nullptr, 0));
   }
-  CG_TRY(cudaMemcpyAsync(p, r, vb, cudaMemcpyDeviceToDevice, st));
+  if (vb) CG_TRY(cudaMemcpyAsync(p, r, vb, cudaMemcpyDeviceToDevice, st));
   CG_TRY(cudaGetLastError());
   CG_TRY(cudaStreamSynchronize(st));
   const double t_setup = now_s();
 
   const int batch = cfg->check_every > 0 ? cfg->check_every : 32;
+  const int ub = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
   auto enqueue_iter = [&]() -> int {
-    int e = launch_spmv(ctx, A, order, p, nullptr, q, nullptr, st);
+    int e = apply(q);
     if (e) return e;
-    cg_reduce_kernel<K, 0><<<G, DOT_THREADS, 0, st>>>(dst, POST_SIGMA, n, p, q, nullptr, nullptr, part, 1);
-    cg_reduce_kernel<K, 1><<<G, DOT_THREADS, 0, st>>>(dst, POST_RHO, n, p, q, x, r, part, 1);
-    const int ub = (int)std::min<int64_t>(148 * 8, (n + 255) / 256);
+    if ((e = reduce(Dot{}, POST_SIGMA, p, q, nullptr, nullptr, 1))) return e;
+    if ((e = reduce(Upd{}, POST_RHO, p, q, x, r, 1))) return e;
     cg_update_p_kernel<K><<<ub, 256, 0, st>>>(dst, n, r, p);
-    return cudaGetLastError() == cudaSuccess ? MPSG_OK : MPSG_E_CUDA;
+    return cudaGetLastError() == cudaSuccess ? MPSG_OK : fail(ctx, MPSG_E_CUDA, "cg: update launch failed");
   };
   int status = CG_RUNNING;
   long long done_k = 0;
@@ -89,8 +145,6 @@ int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, co
     CG_TRY(cudaMemcpy(&hs, &dst->status, sizeof(int), cudaMemcpyDeviceToHost));
     status = hs;
   }
-  cudaGraphExec_t gexec = nullptr;
-  cudaGraph_t graph = nullptr;
   int gbatch = 0;
   while (status == CG_RUNNING) {
     long long remaining = max_iters - done_k;
@@ -108,18 +162,14 @@ int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, co
         cudaError_t ce = cudaStreamEndCapture(st, &graph);
         if (e != MPSG_OK || ce != cudaSuccess) {
           cleanup();
-          return fail(ctx, MPSG_E_CUDA, "cg: graph capture failed (%s)", cudaGetErrorString(ce));
+          return e != MPSG_OK ? e : fail(ctx, MPSG_E_CUDA, "cg: graph capture failed (%s)", cudaGetErrorString(ce));
         }
         CG_TRY(cudaGraphInstantiate(&gexec, graph, 0));
         gbatch = nb;
       }
       CG_TRY(cudaGraphLaunch(gexec, st));
     } else {
-      for (int i = 0; i < nb; ++i)
-        if ((rc = enqueue_iter()) != MPSG_OK) {
-          cleanup();
-          return fail(ctx, rc, "cg: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-        }
+      for (int i = 0; i < nb; ++i) CG_RC(enqueue_iter());
     }
     done_k += nb;
     int hs;
@@ -127,22 +177,16 @@ int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, co
     CG_TRY(cudaStreamSynchronize(st));
     status = hs;
   }
-  if (gexec) cudaGraphExecDestroy(gexec);
-  if (graph) cudaGraphDestroy(graph);
   CgState<K> hst;
   CG_TRY(cudaMemcpy(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost));
   const double t_solve = now_s();
   // Iteration count semantics (krylov.hpp:251-253, 262-268, 276).
-  int64_t iters = hst.k;
-  int fstatus = hst.status == CG_RUNNING ? MPSG_MAX_ITERATIONS : hst.status;
-  if (hst.status == 2 && hst.reason == 1) iters = hst.k;  // breakdown before step k+1
-  // final true residual ||b - A x|| (krylov.hpp:227-232)
-  if ((rc = launch_spmv(ctx, A, order, x, nullptr, q, nullptr, st)) != MPSG_OK) {
-    cleanup();
-    return rc;
-  }
-  cg_reduce_kernel<K, 2><<<G, DOT_THREADS, 0, st>>>(dst, POST_TRUE, n, b, nullptr, q, nullptr, part, 0);
-  CG_TRY(cudaGetLastError());
+  const int64_t iters = hst.k;
+  const int fstatus = hst.status == CG_RUNNING ? MPSG_MAX_ITERATIONS : hst.status;
+  // final true residual ||b - A x|| (krylov.hpp:227-232): x through p's buffer
+  if (vb) CG_TRY(cudaMemcpyAsync(p, x, vb, cudaMemcpyDeviceToDevice, st));
+  CG_RC(apply(q));
+  CG_RC(reduce(Res{}, POST_TRUE, b, nullptr, q, nullptr, 0));
   double true_res = 0.0;
   CG_TRY(cudaMemcpyAsync(&true_res, &dst->true_residual, sizeof(double), cudaMemcpyDeviceToHost, st));
   const int64_t nh = iters + 1;
@@ -151,7 +195,7 @@ int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, co
     CG_TRY(cudaMemcpyAsync(history, hist, (size_t)ncopy * sizeof(double), cudaMemcpyDeviceToHost, st));
   double last_hist = 0.0;
   CG_TRY(cudaMemcpyAsync(&last_hist, hist + (nh - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (x_out) CG_TRY(cudaMemcpyAsync(x_out, x, vb, cudaMemcpyDeviceToHost, st));
+  if (x_out && vb) CG_TRY(cudaMemcpyAsync(x_out, x, vb, cudaMemcpyDeviceToHost, st));
   CG_TRY(cudaStreamSynchronize(st));
   cleanup();
 
@@ -170,11 +214,25 @@ int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, co
   std::snprintf(rep->detail, sizeof(rep->detail), "%s", detail);
   return MPSG_OK;
 #undef CG_TRY
+#undef CG_RC
 }
 
+template <int K>
+int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, const double* x0,
+           const mpsg_cg_config* cfg, double* x_out, double* history, int64_t history_cap, mpsg_cg_report* rep) {
+  return cg_driver<K>(ctx, A, nullptr, order, b_host, x0, cfg, x_out, history, history_cap, rep);
+}
+
+template <int K>
+int run_dcg(mpsg_dcsr* D, int order, const double* b_host, const double* x0, const mpsg_cg_config* cfg,
+            double* x_out, double* history, int64_t history_cap, mpsg_cg_report* rep) {
+  return cg_driver<K>(D->comm->ctx, D->local, D, order, b_host, x0, cfg, x_out, history, history_cap, rep);
+}
 
 }  // namespace mpsg
 
-#define MPSG_INSTANTIATE_CG(K)                                                                 \
-  template int mpsg::run_cg<K>(mpsg_ctx*, const mpsg_csr*, int, const double*, const double*,   \
-                               const mpsg_cg_config*, double*, double*, int64_t, mpsg_cg_report*);
+#define MPSG_INSTANTIATE_CG(K)                                                                            \
+  template int mpsg::run_cg<K>(mpsg_ctx*, const mpsg_csr*, int, const double*, const double*,              \
+                               const mpsg_cg_config*, double*, double*, int64_t, mpsg_cg_report*);         \
+  template int mpsg::run_dcg<K>(mpsg_dcsr*, int, const double*, const double*, const mpsg_cg_config*,      \
+                                double*, double*, int64_t, mpsg_cg_report*);

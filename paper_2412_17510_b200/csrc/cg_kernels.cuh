@@ -119,11 +119,14 @@ MPSG_DI void cg_post(CgState<K>* st, int post, const MC<K>& d) {
 //   0: d += u_i * v_i                                   (dots)
 //   1: x_i += alpha p_i; r_i += (-alpha) q_i; d += r_i r_i (axpy pair + dot)
 //   2: w_i = b_i - w_i; d += w_i w_i                    (true residual)
+// local_out != nullptr (multi-GPU): the last block stores this rank's total
+// there instead of running the scalar step; cg_post_gathered_kernel finishes
+// after the partials of all ranks are allgathered.
 template <int K, int MODE>
 __global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, int post, int64_t n,
                                                                 const double* u, const double* v,
                                                                 double* x, double* r, double* partial,
-                                                                int gate) {
+                                                                int gate, double* local_out) {
   __shared__ MC<K> sh[DOT_THREADS / 32];
   __shared__ bool last;
   if (gate && st->status != CG_RUNNING) return;
@@ -179,8 +182,23 @@ __global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, 
   MC<K> tot = block_reduce(s, sh);
   if (threadIdx.x == 0) {
     st->ticket = 0u;
-    cg_post(st, post, tot);
+    if (local_out) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) local_out[j] = tot.c[j];
+    } else {
+      cg_post(st, post, tot);
+    }
   }
+}
+
+// Rank-ordered multi-component sum of the allgathered partials, then the
+// scalar step -- the same on every rank.
+template <int K>
+__global__ void cg_post_gathered_kernel(CgState<K>* st, int post, const double* gathered, int nranks, int gate) {
+  if (gate && st->status != CG_RUNNING) return;
+  MC<K> s = zero<K>();
+  for (int q = 0; q < nranks; ++q) s = add(s, load_aos_rw<K>(gathered, q));
+  cg_post(st, post, s);
 }
 
 // p = r + beta p (krylov.hpp:272)

@@ -1,0 +1,301 @@
+// dist.cu -- C ABI of the row-sharded multi-GPU layer (see dist.h).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "dist.h"
+
+using namespace mpsg;
+
+namespace mpsg {
+
+const NcclApi* NcclApi::get(std::string* err) {
+  static NcclApi api;
+  static bool ok = false;
+  static std::string why;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    bool all = true;
+    auto sym = [&](auto& fp, const char* name) {
+      fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+      if (!fp) all = false;
+    };
+    sym(api.GetUniqueId, "ncclGetUniqueId");
+    sym(api.CommInitRank, "ncclCommInitRank");
+    sym(api.CommDestroy, "ncclCommDestroy");
+    sym(api.Send, "ncclSend");
+    sym(api.Recv, "ncclRecv");
+    sym(api.AllGather, "ncclAllGather");
+    sym(api.GroupStart, "ncclGroupStart");
+    sym(api.GroupEnd, "ncclGroupEnd");
+    sym(api.GetErrorString, "ncclGetErrorString");
+    if (!all)
+      why = "libnccl.so.2 lacks a required symbol";
+    else
+      ok = true;
+  });
+  if (!ok && err) *err = why;
+  return ok ? &api : nullptr;
+}
+
+int halo_exchange(const mpsg_dcsr* A, double* xfull, cudaStream_t st) {
+  const mpsg_comm* c = A->comm;
+  if (c->nranks == 1 || A->halo_rows == 0) return MPSG_OK;
+  const int K = A->K;
+  NCCL_TRY(c, c->api->GroupStart());
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) continue;
+    const int64_t slo = A->send[2 * q], shi = A->send[2 * q + 1];
+    const int64_t rlo = A->recv[2 * q], rhi = A->recv[2 * q + 1];
+    if (shi > slo)
+      NCCL_TRY(c, c->api->Send(xfull + slo * K, (size_t)(shi - slo) * K, ncclDouble, q, c->comm, st));
+    if (rhi > rlo)
+      NCCL_TRY(c, c->api->Recv(xfull + rlo * K, (size_t)(rhi - rlo) * K, ncclDouble, q, c->comm, st));
+  }
+  NCCL_TRY(c, c->api->GroupEnd());
+  return MPSG_OK;
+}
+
+int allgather_mc(const mpsg_comm* c, const double* in, double* out, int K, cudaStream_t st) {
+  if (c->nranks == 1) {
+    CUDA_TRY(c->ctx, cudaMemcpyAsync(out, in, (size_t)K * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return MPSG_OK;
+  }
+  NCCL_TRY(c, c->api->AllGather(in, out, (size_t)K, ncclDouble, c->comm, st));
+  return MPSG_OK;
+}
+
+}  // namespace mpsg
+
+namespace {
+
+void free_dcsr(mpsg_dcsr* A) {
+  if (!A) return;
+  mpsg_csr_destroy(A->local);
+  for (double* p : {A->xfull[0], A->xfull[1], A->ybuf[0], A->ybuf[1]})
+    if (p) cudaFree(p);
+  delete A;
+}
+
+// Own block of a distributed vector into the global-length buffer, then halo.
+int stage_x(mpsg_dcsr* A, const double* x_local, double* xfull, cudaMemcpyKind kind, cudaStream_t st) {
+  const size_t b = (size_t)(A->row_end - A->row_begin) * A->K * sizeof(double);
+  if (b) CUDA_TRY(A->comm->ctx, cudaMemcpyAsync(xfull + A->row_begin * A->K, x_local, b, kind, st));
+  return halo_exchange(A, xfull, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int mpsg_halo_plan(int nranks, int rank, const int64_t* bounds, const int64_t* need, int64_t* send,
+                   int64_t* recv) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !bounds || !need || !send || !recv) return MPSG_E_ARG;
+  for (int q = 0; q < nranks; ++q) {
+    // what rank q reads of my rows / what I read of q's rows
+    int64_t slo = std::max(need[2 * q], bounds[rank]), shi = std::min(need[2 * q + 1], bounds[rank + 1]);
+    int64_t rlo = std::max(need[2 * rank], bounds[q]), rhi = std::min(need[2 * rank + 1], bounds[q + 1]);
+    if (q == rank || shi <= slo) slo = shi = 0;
+    if (q == rank || rhi <= rlo) rlo = rhi = 0;
+    send[2 * q] = slo;
+    send[2 * q + 1] = shi;
+    recv[2 * q] = rlo;
+    recv[2 * q + 1] = rhi;
+  }
+  return MPSG_OK;
+}
+
+int mpsg_comm_unique_id(unsigned char* id) {
+  if (!id) return MPSG_E_ARG;
+  std::string err;
+  const NcclApi* api = NcclApi::get(&err);
+  if (!api) return MPSG_E_NCCL;
+  ncclUniqueId u;
+  if (api->GetUniqueId(&u) != ncclSuccess) return MPSG_E_NCCL;
+  std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  return MPSG_OK;
+}
+
+int mpsg_comm_create(mpsg_ctx* ctx, int nranks, int rank, const unsigned char* id, mpsg_comm** out) {
+  if (!ctx || !out || nranks < 1 || rank < 0 || rank >= nranks) return MPSG_E_ARG;
+  *out = nullptr;
+  auto* c = new mpsg_comm();
+  c->ctx = ctx;
+  c->nranks = nranks;
+  c->rank = rank;
+  if (nranks > 1) {
+    if (!id) {
+      delete c;
+      return fail(ctx, MPSG_E_ARG, "comm_create: a unique id is required for nranks > 1");
+    }
+    std::string err;
+    c->api = NcclApi::get(&err);
+    if (!c->api) {
+      delete c;
+      return fail(ctx, MPSG_E_NCCL, "comm_create: %s", err.c_str());
+    }
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+    cudaSetDevice(ctx->device);
+    ncclResult_t r = c->api->CommInitRank(&c->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+      const char* s = c->api->GetErrorString(r);
+      delete c;
+      return fail(ctx, MPSG_E_NCCL, "ncclCommInitRank: %s", s);
+    }
+  }
+  *out = c;
+  return MPSG_OK;
+}
+
+void mpsg_comm_destroy(mpsg_comm* c) {
+  if (!c) return;
+  if (c->comm && c->api) c->api->CommDestroy(c->comm);
+  delete c;
+}
+
+int mpsg_dcsr_upload(mpsg_comm* c, int K, int is_complex, int64_t nglobal, int64_t row_begin, int64_t row_end,
+                     const int64_t* indptr, const int64_t* indices, const double* const* planes, mpsg_dcsr** out) {
+  if (!c || !out || !indptr) return MPSG_E_ARG;
+  *out = nullptr;
+  mpsg_ctx* ctx = c->ctx;
+  if (row_begin < 0 || row_end < row_begin || row_end > nglobal)
+    return fail(ctx, MPSG_E_ARG, "dcsr_upload: bad row block [%lld, %lld) of %lld", (long long)row_begin,
+                (long long)row_end, (long long)nglobal);
+  const int64_t nloc = row_end - row_begin;
+  auto* A = new mpsg_dcsr();
+  std::unique_ptr<mpsg_dcsr, void (*)(mpsg_dcsr*)> holder(A, free_dcsr);
+  A->comm = c;
+  A->K = K;
+  A->cplx = is_complex != 0;
+  A->nglobal = nglobal;
+  A->row_begin = row_begin;
+  A->row_end = row_end;
+  int rc = mpsg_csr_upload(ctx, K, is_complex, nloc, nglobal, indptr, indices, planes, &A->local);
+  if (rc) return rc;
+  // the column interval this rank reads (its own block is always local)
+  int64_t lo = row_begin, hi = row_end;
+  const int64_t nnz = indptr[nloc];
+  for (int64_t k = 0; k < nnz; ++k) {
+    lo = std::min(lo, indices[k]);
+    hi = std::max(hi, indices[k] + 1);
+  }
+  // every rank's row block and read interval (tiny allgather at setup)
+  const int P = c->nranks;
+  std::vector<int64_t> mine = {row_begin, row_end, lo, hi}, all((size_t)4 * P);
+  if (P == 1) {
+    all = mine;
+  } else {
+    int64_t* d = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(&d, sizeof(int64_t) * 4 * (P + 1)));
+    cudaStream_t st = ctx->stream;
+    cudaMemcpyAsync(d, mine.data(), sizeof(int64_t) * 4, cudaMemcpyHostToDevice, st);
+    ncclResult_t r = c->api->AllGather(d, d + 4, 4, ncclInt64, c->comm, st);
+    cudaMemcpyAsync(all.data(), d + 4, sizeof(int64_t) * 4 * P, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    if (r != ncclSuccess) return fail(ctx, MPSG_E_NCCL, "dcsr_upload allgather: %s", c->api->GetErrorString(r));
+    if (e != cudaSuccess) return fail(ctx, MPSG_E_CUDA, "dcsr_upload: %s", cudaGetErrorString(e));
+  }
+  A->bounds.assign((size_t)P + 1, 0);
+  A->need.assign((size_t)2 * P, 0);
+  for (int q = 0; q < P; ++q) {
+    if (all[4 * q] != A->bounds[q])
+      return fail(ctx, MPSG_E_ARG, "dcsr_upload: row blocks are not contiguous in rank order");
+    A->bounds[q + 1] = all[4 * q + 1];
+    A->need[2 * q] = all[4 * q + 2];
+    A->need[2 * q + 1] = all[4 * q + 3];
+  }
+  if (A->bounds[P] != nglobal) return fail(ctx, MPSG_E_ARG, "dcsr_upload: row blocks do not cover the matrix");
+  A->send.assign((size_t)2 * P, 0);
+  A->recv.assign((size_t)2 * P, 0);
+  mpsg_halo_plan(P, c->rank, A->bounds.data(), A->need.data(), A->send.data(), A->recv.data());
+  for (int q = 0; q < P; ++q) A->halo_rows += A->recv[2 * q + 1] - A->recv[2 * q];
+  const size_t xb = (size_t)std::max<int64_t>(nglobal, 1) * K * sizeof(double);
+  for (int j = 0; j < (A->cplx ? 2 : 1); ++j) {
+    CUDA_TRY(ctx, cudaMalloc(&A->xfull[j], xb));
+    CUDA_TRY(ctx, cudaMemset(A->xfull[j], 0, xb));
+  }
+  *out = holder.release();
+  return MPSG_OK;
+}
+
+void mpsg_dcsr_destroy(mpsg_dcsr* A) { free_dcsr(A); }
+
+int mpsg_dcsr_info(const mpsg_dcsr* A, int64_t* bounds, int64_t* halo_rows) {
+  if (!A) return MPSG_E_ARG;
+  if (bounds) std::copy(A->bounds.begin(), A->bounds.end(), bounds);
+  if (halo_rows) *halo_rows = A->halo_rows;
+  return MPSG_OK;
+}
+
+int mpsg_dspmv_dev(mpsg_dcsr* A, int order, const double* d_x_local, double* d_y_local, void* stream) {
+  if (!A) return MPSG_E_ARG;
+  if (A->cplx) return fail(A->comm->ctx, MPSG_E_ARG, "dspmv: matrix is complex, use mpsg_dspmv_complex_dev");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : A->comm->ctx->stream;
+  int rc = stage_x(A, d_x_local, A->xfull[0], cudaMemcpyDeviceToDevice, st);
+  if (rc) return rc;
+  return launch_spmv(A->comm->ctx, A->local, order, A->xfull[0], nullptr, d_y_local, nullptr, st);
+}
+
+int mpsg_dspmv_complex_dev(mpsg_dcsr* A, int order, const double* d_xr_local, const double* d_xi_local,
+                           double* d_yr_local, double* d_yi_local, void* stream) {
+  if (!A) return MPSG_E_ARG;
+  if (!A->cplx) return fail(A->comm->ctx, MPSG_E_ARG, "dspmv_complex: matrix is real");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : A->comm->ctx->stream;
+  int rc = stage_x(A, d_xr_local, A->xfull[0], cudaMemcpyDeviceToDevice, st);
+  if (!rc) rc = stage_x(A, d_xi_local, A->xfull[1], cudaMemcpyDeviceToDevice, st);
+  if (rc) return rc;
+  return launch_spmv(A->comm->ctx, A->local, order, A->xfull[0], A->xfull[1], d_yr_local, d_yi_local, st);
+}
+
+int mpsg_dspmv(mpsg_dcsr* A, int order, const double* x_local, double* y_local) {
+  if (!A) return MPSG_E_ARG;
+  mpsg_ctx* ctx = A->comm->ctx;
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "dspmv: matrix is complex, use mpsg_dspmv_complex_dev");
+  const int64_t nloc = A->row_end - A->row_begin;
+  const size_t b = (size_t)nloc * A->K * sizeof(double);
+  const int ns = A->cplx ? 2 : 1;
+  for (int j = 0; j < ns; ++j)
+    if (!A->ybuf[j]) CUDA_TRY(ctx, cudaMalloc(&A->ybuf[j], b ? b : 8));
+  cudaStream_t st = ctx->stream;
+  int rc = stage_x(A, x_local, A->xfull[0], cudaMemcpyHostToDevice, st);
+  if (rc) return rc;
+  if ((rc = launch_spmv(ctx, A->local, order, A->xfull[0], nullptr, A->ybuf[0], nullptr, st))) return rc;
+  if (b) CUDA_TRY(ctx, cudaMemcpyAsync(y_local, A->ybuf[0], b, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MPSG_OK;
+}
+
+int mpsg_dcg(mpsg_dcsr* A, int order, const double* b_local, const double* x0_local, const mpsg_cg_config* cfg,
+             double* x_out_local, double* history, int64_t history_cap, mpsg_cg_report* report) {
+  if (!A || !cfg || !report || (!b_local && A->row_end > A->row_begin)) return MPSG_E_ARG;
+  mpsg_ctx* ctx = A->comm->ctx;
+  if (!(cfg->rel_tol > 0.0) || !(cfg->abs_tol > 0.0))
+    return fail(ctx, MPSG_E_ARG, "solver: tolerances must be positive");
+  if (cfg->max_iters < 1) return fail(ctx, MPSG_E_ARG, "solver: max_iters must be at least 1");
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "solver: complex matrices are not supported by cg");
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "cg: unknown order %d", order);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  switch (A->K) {
+    case 2: return run_dcg<2>(A, order, b_local, x0_local, cfg, x_out_local, history, history_cap, report);
+    case 3: return run_dcg<3>(A, order, b_local, x0_local, cfg, x_out_local, history, history_cap, report);
+    case 4: return run_dcg<4>(A, order, b_local, x0_local, cfg, x_out_local, history, history_cap, report);
+  }
+  return fail(ctx, MPSG_E_ARG, "cg: unsupported K");
+}
+
+}  // extern "C"

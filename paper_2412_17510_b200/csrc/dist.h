@@ -1,0 +1,87 @@
+// dist.h -- row-sharded multi-GPU layer (one process per GPU, NCCL over
+// NVLink/NVSwitch).  Internal to the library; the ABI is in include/mpsg.h.
+//
+// Shard rule: rank r owns the contiguous row block [bounds[r], bounds[r+1])
+// chosen by the reference's partition_rows (kernels.hpp:63-80: equal nnz), and
+// the matching block of x and y (square matrices).  Rows never split, so the
+// exact orders (SCALAR / LANE4) stay bit-exact under any partition.
+//
+// Per SpMV the only traffic is the x halo: each rank needs the column interval
+// [need_lo, need_hi) its rows touch; the parts owned by other ranks arrive by
+// ncclSend/ncclRecv pairs in one group (neighbour halo for banded/stencil
+// matrices, all-to-all blocks -- an allgather -- for unstructured ones) into a
+// global-length x buffer indexed by global column, so the local kernels are
+// the single-GPU kernels unchanged.
+// Dot products in CG: each rank reduces its rows to one K-component partial,
+// the partials are allgathered (P*K doubles) and summed in rank order with the
+// multi-component add on every rank -- identical and deterministic everywhere
+// (an ncclSum of doubles would destroy the multi-component exactness).
+#pragma once
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace mpsg {
+
+// NCCL is resolved at run time (dlopen of libnccl.so.2, the library torch has
+// usually loaded already), so single-GPU use never depends on it.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+  static const NcclApi* get(std::string* err);
+};
+
+}  // namespace mpsg
+
+struct mpsg_comm {
+  mpsg_ctx* ctx = nullptr;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  const mpsg::NcclApi* api = nullptr;
+};
+
+struct mpsg_dcsr {
+  mpsg_comm* comm = nullptr;
+  mpsg_csr* local = nullptr;  // this rank's rows, global column indices
+  int K = 2;
+  bool cplx = false;
+  int64_t nglobal = 0, row_begin = 0, row_end = 0;
+  std::vector<int64_t> bounds;  // [nranks+1] row ownership
+  std::vector<int64_t> need;    // [2*nranks] column interval each rank reads
+  std::vector<int64_t> send;    // [2*nranks] my rows peer q reads (lo, hi)
+  std::vector<int64_t> recv;    // [2*nranks] q's rows I read (lo, hi)
+  double* xfull[2] = {nullptr, nullptr};  // global-length x (re, im)
+  double* ybuf[2] = {nullptr, nullptr};   // local y scratch (host-pointer calls)
+  int64_t halo_rows = 0;                  // rows received per SpMV
+};
+
+namespace mpsg {
+
+#define NCCL_TRY(cm, call)                                                                  \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail((cm)->ctx, MPSG_E_NCCL, "%s: %s", #call, (cm)->api->GetErrorString(r_)); \
+  } while (0)
+
+// Exchange the halo of a global-length buffer whose own block is in place.
+int halo_exchange(const mpsg_dcsr* A, double* xfull, cudaStream_t st);
+// out[P*K] = every rank's in[K] (rank order).
+int allgather_mc(const mpsg_comm* c, const double* in, double* out, int K, cudaStream_t st);
+
+// Distributed device CG (cg_inst.cuh), b / x0 / x_out are this rank's block.
+template <int K>
+int run_dcg(mpsg_dcsr* A, int order, const double* b_host, const double* x0, const mpsg_cg_config* cfg,
+            double* x_out, double* history, int64_t history_cap, mpsg_cg_report* rep);
+
+}  // namespace mpsg

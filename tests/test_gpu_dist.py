@@ -1,0 +1,88 @@
+"""Row-sharded path (mpsg_comm / mpsg_dcsr) on one B200.
+
+Only one GPU is available to the tests, so the NCCL layer runs as a one-rank
+group: the shard is the whole matrix, the halo plan is empty, and the results
+must equal the single-GPU path -- bit for bit for SpMV, iteration for
+iteration for CG.  The multi-rank host logic (partition, plan, exchange) is
+pinned on CPU by tests/test_dist_cpu.py.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2412_17510_b200 as M
+import synth
+from tests.util import bits_equal
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = M.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("cfg,K,p1,p2,p3", [(4, 2, 20000, 5000.0, 1.8), (5, 4, 24, 0.0, 0.0), (2, 3, 5000, 32.0, 0.0)])
+@pytest.mark.parametrize("order", [0, 1])
+def test_one_rank_dspmv_equals_spmv(ctx, cfg, K, p1, p2, p3, order):
+    A = synth.config_matrix(cfg, K, p1, p2, p3)
+    x = synth.config_vector(cfg, A.nrows, K)
+    comm = M.Comm(ctx, 1, 0)
+    dA = M.DistCsr.from_global(comm, A, K)
+    bounds, halo = dA.info()
+    assert bounds.tolist() == [0, A.nrows] and halo == 0
+    y = M.dspmv(dA, x, order)
+    assert bits_equal(y, O.spmv(A, x, order))
+    dA.close()
+    comm.close()
+
+
+def test_one_rank_dspmv_complex_dev(ctx):
+    import torch
+
+    K = 4
+    A = synth.config_matrix(3, K, 2000, 16.0)
+    xr, xi = synth.config_vector(3, A.nrows, K)
+    comm = M.Comm(ctx, 1, 0)
+    dA = M.DistCsr.from_global(comm, A, K, is_complex=True)
+    dxr, dxi = torch.from_numpy(xr).cuda(), torch.from_numpy(xi).cuda()
+    dyr, dyi = torch.empty_like(dxr), torch.empty_like(dxi)
+    M.dspmv_complex_dev(dA, dxr.data_ptr(), dxi.data_ptr(), dyr.data_ptr(), dyi.data_ptr(), M.ORDER_LANE4)
+    ctx.synchronize()
+    rr, ri = O.spmv_complex(A, xr, xi, 1)
+    assert bits_equal(dyr.cpu().numpy(), rr) and bits_equal(dyi.cpu().numpy(), ri)
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_one_rank_dcg_tracks_single_gpu_cg(ctx, K):
+    A = synth.config_matrix(5, K, 20)
+    xt = synth.config_vector(5, A.nrows, K)
+    b = O.spmv(A, xt, 1)
+    cfg = M.SolverConfig(rel_tol=1e-25, max_iters=300)
+    single = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, K, ctx=ctx)), b, cfg)
+    comm = M.Comm(ctx, 1, 0)
+    dA = M.DistCsr.from_global(comm, A, K)
+    dist = M.dsolve_cg(dA, b, cfg)
+    assert dist.report.status == single.report.status
+    assert abs(dist.report.iterations - single.report.iterations) <= 1
+    h1, h2 = np.array(single.report.residual_history), np.array(dist.report.residual_history)
+    n = min(len(h1), len(h2))
+    assert np.allclose(h1[:n], h2[:n], rtol=1e-10, atol=0)
+    assert dist.report.final_true_residual <= 10 * single.report.final_true_residual + 1e-30
+
+
+def test_one_rank_dcg_with_initial_guess_and_graph_off(ctx):
+    K = 2
+    A = synth.config_matrix(5, K, 12)
+    xt = synth.config_vector(5, A.nrows, K)
+    b = O.spmv(A, xt, 1)
+    x0 = list(np.linspace(-1, 1, A.nrows))
+    comm = M.Comm(ctx, 1, 0)
+    dA = M.DistCsr.from_global(comm, A, K)
+    r1 = M.dsolve_cg(dA, b, M.SolverConfig(rel_tol=1e-20, max_iters=200, x0=x0, use_graph=False))
+    r2 = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, K, ctx=ctx)), b, M.SolverConfig(rel_tol=1e-20, max_iters=200, x0=x0))
+    assert r1.report.converged and r2.report.converged
+    assert abs(r1.report.iterations - r2.report.iterations) <= 1
+    assert np.allclose(r1.x[:, 0], xt[:, 0], atol=1e-12)
