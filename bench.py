@@ -1,21 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark: multi-precision CSR SpMV on B200 (BASELINE.json metric).
+"""Benchmark: multi-precision CSR SpMV / CG on B200 (BASELINE.json metric).
 
 Default workload (N=1): BASELINE.json configs[1] -- real QD CSR SpMV on the
 random Poisson(32) matrix, n = 1,000,000 (nnz ~ 32.0M), seeded synthetic
-inputs; the TD variant of the same config is reported beside it.  One step =
-one y = A x over the whole matrix.
+inputs, FAST order; the TD variant of the same config is reported beside it.
+One step = one y = A x over the whole matrix.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
-                    [--config cfg2] [--K 4] [--order fast|lane4|scalar] [--all]
+                    [--config cfg1..cfg5] [--K 2|3|4] [--order fast|lane4|scalar]
+                    [--shard] [--cg] [--all]
 
-Under torchrun (N > 1) every rank runs its own replica of the single-GPU
-config (configs[1] does not shard: "replicas only", weak scaling); timing is
-the max over ranks of the device-timed region.
+Multi-GPU (torchrun, one process per GPU):
+  * default (cfg2, a single-GPU config in BASELINE.json): every rank runs its
+    own replica ("replicas only", weak scaling);
+  * --shard (the sharded configs 3, 4, 5): the matrix is row-sharded by equal
+    nnz across the ranks, x halos move over NCCL (strong scaling: value = the
+    whole matrix's nnz / the max-over-ranks step time);
+  * --cg (config 5): 500-iteration CG, row-sharded with --shard.
 
 `--impl reference` times the reference's own CPU implementation (the
-unmodified reference compiled from /root/reference into oracle/_ref, run with
-all host threads) on the same config; rank 0 only.
+unmodified reference compiled from /root/reference into oracle/_ref, all host
+threads) on the same workload; rank 0 only.
 """
 from __future__ import annotations
 
@@ -47,6 +52,7 @@ CONFIG_DESC = {
 # sequence (counted with the reference's templated chains)
 OPS_PER_NNZ = {2: 20, 3: 202, 4: 206}
 K_NAME = {2: "DD", 3: "TD", 4: "QD"}
+CG_ITERS = 500
 
 
 def algorithmic_bytes(nnz, n, K, cplx):
@@ -59,13 +65,30 @@ def algorithmic_ops(nnz, K, cplx):
     return nnz * OPS_PER_NNZ[K] * (4 if cplx else 1)
 
 
+def cg_iter_bytes(nnz, n, K):
+    # SpMV + x, r, p read/write + q write/read
+    return nnz * (8 * K + 4) + 4 * (n + 1) + 11 * n * 8 * K
+
+
+def cg_iter_ops(nnz, n, K):
+    return (nnz + 5 * n) * OPS_PER_NNZ[K]
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d.get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json"
+        return float(d.get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json (copy kernel)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(key):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(key)
+    return None
 
 
 class ClockSampler:
@@ -87,6 +110,7 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.3)
         except Exception:
             self.proc = None
 
@@ -126,92 +150,140 @@ def make_inputs(cfg: str, K: int):
 
 
 # --------------------------------------------------------------------------- reference arm
-def run_reference(args, cfg, K, sample_rows=None):
-    """Time the unmodified reference spmv (oracle/_ref) on host cores."""
+def run_reference(steps, warmup, cfg, K, cg=False, threads=None):
+    """Time the unmodified reference (oracle/_ref: mps::spmv / mps::solve_cg) on host cores."""
     import oracle as O
 
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     A, x = make_inputs(cfg, K)
     cplx = cfg == "cfg3"
     kind = "reference" if O.ref_available() else "port"
-    if sample_rows and sample_rows < A.nrows:
-        from types import SimpleNamespace
-
-        nnz_s = int(A.indptr[sample_rows])
-        A = SimpleNamespace(nrows=sample_rows, ncols=A.ncols, indptr=A.indptr[: sample_rows + 1],
-                            indices=A.indices[:nnz_s], planes=A.planes[:, :nnz_s], K=K, nnz=nnz_s)
-    nnz = int(A.indptr[A.nrows])
     order = 1  # lanes on: the reference default (kernels.hpp:44)
-    times = []
-    if kind == "reference":
-        if cplx:
-            Ah, xh, yh = O.RefComplex(A, K), O.RefCVec(*x), O.RefCVec(K=K)
-            call = lambda: O.ref().ref_spmv_complex(Ah.h, xh.h, order, threads, yh.h)  # noqa: E731
+    nnz = A.nnz
+    if cg:
+        # a bounded prefix of the 500-iteration solve (the serial vector ops of
+        # krylov.hpp:122-140 dominate; the full run is minutes to tens of minutes)
+        iters = 3
+        if kind == "reference":
+            b = O.ref_spmv(A, x, order, threads=threads)
+            call = lambda: O.ref_cg(A, b, order, threads=threads, rel_tol=1e-30, max_iters=iters)  # noqa: E731
         else:
-            Ah, xh, yh = O.RefCsr(A, K), O.RefVec(x), O.RefVec(K=K)
-            call = lambda: O.ref().ref_spmv(Ah.h, xh.h, order, threads, yh.h)  # noqa: E731
-        threads_used = threads
+            threads = 1
+            b = O.spmv(A, x, order)
+            call = lambda: O.cg(A, b, order, rel_tol=1e-30, max_iters=iters)  # noqa: E731
+        units = nnz * iters
+        sample = (f"cfg5 {K_NAME[K]} CG, first {iters} of {CG_ITERS} iterations (SpMV on {threads} OpenMP "
+                  f"threads, vector ops serial as in krylov.hpp:122-140)")
     else:
-        call = (lambda: O.spmv_complex(A, x[0], x[1], order)) if cplx else (lambda: O.spmv(A, x, order))
-        threads_used = 1
-    for _ in range(args.warmup):
+        if kind == "reference":
+            if cplx:
+                Ah, xh, yh = O.RefComplex(A, K), O.RefCVec(*x), O.RefCVec(K=K)
+                call = lambda: O.ref().ref_spmv_complex(Ah.h, xh.h, order, threads, yh.h)  # noqa: E731
+            else:
+                Ah, xh, yh = O.RefCsr(A, K), O.RefVec(x), O.RefVec(K=K)
+                call = lambda: O.ref().ref_spmv(Ah.h, xh.h, order, threads, yh.h)  # noqa: E731
+        else:
+            threads = 1
+            call = (lambda: O.spmv_complex(A, x[0], x[1], order)) if cplx else (lambda: O.spmv(A, x, order))
+        units = nnz
+        sample = (f"{cfg} {K_NAME[K]} {'complex ' if cplx else ''}full matrix (nnz={nnz}), lanes on, "
+                  f"{threads} OpenMP threads")
+    for _ in range(warmup):
         call()
-    for _ in range(args.steps):
+    times = []
+    for _ in range(steps):
         t0 = time.perf_counter()
         call()
         times.append(time.perf_counter() - t0)
     med = statistics.median(times)
-    return dict(value=nnz / med / 1e9, seconds=sum(times), median_s=med, cores=threads_used, kind=kind,
-                sample=(f"{cfg} {K_NAME[K]} {'complex ' if cplx else ''}rows [0,{A.nrows}) nnz={nnz}, "
-                        f"lanes on, {threads_used} OpenMP threads, median of {len(times)} calls"))
+    return dict(value=units / med / 1e9, median_s=med, cores=threads, kind=kind,
+                sample=sample + f", median of {len(times)} timed calls after {warmup} warm-up")
 
 
 # --------------------------------------------------------------------------- GPU arm
-def run_gpu(args, cfg, K, order, rank, world, dist):
+class Flush:
+    """L2 flush before a timed step: write a 256 MB buffer (> 126 MB L2), then
+    read a second 256 MB buffer so the write's dirty lines are evicted before
+    the timed launch (the kernel starts with a cold, clean L2)."""
+
+    def __init__(self, torch, dev):
+        self.w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+        self.r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+        self.acc = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def __call__(self):
+        self.w.zero_()
+        self.acc.add_(self.r.sum())
+
+
+def setup_stream(torch, M, dev):
+    # a dedicated (non-default) stream: every launch of ours and every timing
+    # event goes on it (torch's legacy default stream has handle 0, which the C
+    # ABI reads as "the context's own stream")
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = M.Context(dev.index)
+    ctx.set_stream(stream.cuda_stream)
+    return stream, ctx
+
+
+def make_comm(M, ctx, world, rank, dist):
+    uid = [M.Comm.unique_id() if (rank == 0 and world > 1) else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    return M.Comm(ctx, world, rank, uid[0])
+
+
+def max_over_ranks(torch, dev, dist, v):
+    if not dist:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_gpu_spmv(args, cfg, K, order, rank, world, dist):
     import torch
 
     import paper_2412_17510_b200 as M
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    # a dedicated (non-default) stream: every launch of ours and every timing
-    # event goes on it (torch's legacy default stream has handle 0, which the
-    # C ABI reads as "the context's own stream")
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    ctx = M.Context(dev.index)
-    ctx.set_stream(stream.cuda_stream)
+    stream, ctx = setup_stream(torch, M, dev)
     cplx = cfg == "cfg3"
     A, x = make_inputs(cfg, K)
-    dA = M.DeviceCsr(A, K, cplx, ctx=ctx)
-    st = dA.stats()
     n, nnz = A.nrows, A.nnz
-    if cplx:
-        dxr, dxi = torch.from_numpy(x[0]).to(dev), torch.from_numpy(x[1]).to(dev)
-        dyr, dyi = torch.empty((n, K), dtype=torch.float64, device=dev), torch.empty((n, K), dtype=torch.float64,
-                                                                                     device=dev)
-        step = lambda: M.spmv_complex_dev(dA, dxr.data_ptr(), dxi.data_ptr(), dyr.data_ptr(), dyi.data_ptr(),  # noqa
-                                          order, stream.cuda_stream)
+    shard = args.shard and world > 1
+    xs = list(x) if cplx else [x]
+    comm = None
+    if shard:
+        comm = make_comm(M, ctx, world, rank, dist)
+        dA = M.DistCsr.from_global(comm, A, K, cplx)
+        b, e = dA.row_begin, dA.row_end
+        _, halo = dA.info()
+        dxs = [torch.from_numpy(np.ascontiguousarray(v[b:e])).to(dev) for v in xs]
+        dys = [torch.empty((e - b, K), dtype=torch.float64, device=dev) for _ in xs]
+        if cplx:
+            step = lambda: M.dspmv_complex_dev(dA, dxs[0].data_ptr(), dxs[1].data_ptr(), dys[0].data_ptr(),  # noqa
+                                               dys[1].data_ptr(), order, stream.cuda_stream)
+        else:
+            step = lambda: M.dspmv_dev(dA, dxs[0].data_ptr(), dys[0].data_ptr(), order, stream.cuda_stream)  # noqa
+        local_stats = None
+        units = nnz  # strong scaling: the whole matrix per step across the group
     else:
-        dx = torch.from_numpy(x).to(dev)
-        dy = torch.empty((n, K), dtype=torch.float64, device=dev)
-        step = lambda: M.spmv_dev(dA, dx.data_ptr(), dy.data_ptr(), order, stream.cuda_stream)  # noqa: E731
-    # L2 flush between timed steps: write a 256 MB buffer (> 126 MB L2), then
-    # read a second 256 MB buffer so the dirty lines of the write are evicted
-    # before the timed launch (the kernel starts with a cold, clean L2 instead
-    # of paying for the flush's write-backs)
-    flush_w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-    flush_r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-    flush_acc = torch.zeros(1, dtype=torch.int64, device=dev)
-
-    class _Flush:
-        @staticmethod
-        def zero_():
-            flush_w.zero_()
-            flush_acc.add_(flush_r.sum())
-
-    flush = _Flush()
+        dA = M.DeviceCsr(A, K, cplx, ctx=ctx)
+        local_stats = dA.stats()
+        halo = 0
+        dxs = [torch.from_numpy(v).to(dev) for v in xs]
+        dys = [torch.empty((n, K), dtype=torch.float64, device=dev) for _ in xs]
+        if cplx:
+            step = lambda: M.spmv_complex_dev(dA, dxs[0].data_ptr(), dxs[1].data_ptr(), dys[0].data_ptr(),  # noqa
+                                              dys[1].data_ptr(), order, stream.cuda_stream)
+        else:
+            step = lambda: M.spmv_dev(dA, dxs[0].data_ptr(), dys[0].data_ptr(), order, stream.cuda_stream)  # noqa
+        units = world * nnz  # replicas (weak scaling)
+    flush = Flush(torch, dev)
     for _ in range(args.warmup):
-        flush.zero_()
+        flush()
         step()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -222,7 +294,7 @@ def run_gpu(args, cfg, K, order, rank, world, dist):
         dist.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
-        flush.zero_()
+        flush()
         starts[i].record(stream)
         step()
         ends[i].record(stream)
@@ -231,18 +303,13 @@ def run_gpu(args, cfg, K, order, rank, world, dist):
         dist.barrier()
     clocks = clk.stop()
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t_total = sum(ms) / 1e3
-    if dist:
-        t = torch.tensor([t_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_total = float(t.item())
-    per_launch = t_total / args.steps
+    t_total = max_over_ranks(torch, dev, dist, sum(ms) / 1e3)
 
     # e2e through the host-pointer C-ABI call (pinned host buffers, H2D + D2H inside)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not shard:
         if cplx:
-            hx = [torch.from_numpy(v).pin_memory() for v in x]
+            hx = [torch.from_numpy(v).pin_memory() for v in xs]
             hy = [torch.empty((n, K), dtype=torch.float64).pin_memory() for _ in range(2)]
             call = lambda: M.lib().mpsg_spmv_complex(ctx.h, dA.h, order, n, hx[0].data_ptr(), hx[1].data_ptr(),  # noqa
                                                      hy[0].data_ptr(), hy[1].data_ptr())
@@ -253,30 +320,114 @@ def run_gpu(args, cfg, K, order, rank, world, dist):
             call = lambda: M.lib().mpsg_spmv(ctx.h, dA.h, order, n, hx.data_ptr(), hy.data_ptr())  # noqa: E731
             h2d, d2h = n * K * 8, n * K * 8
         for _ in range(max(1, args.warmup)):
-            flush.zero_()
+            flush()
             ctx.check(call())
         ets = []
         if dist:
             dist.barrier()
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             ctx.check(call())
             e1.record(stream)
             torch.cuda.synchronize()
             ets.append(e0.elapsed_time(e1) / 1e3)
-        te = sum(ets)
-        if dist:
-            t = torch.tensor([te], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+        te = max_over_ranks(torch, dev, dist, sum(ets))
         e2e = {"value": world * nnz * args.steps / te / 1e9, "unit": "Gnnz/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
-    launches = args.steps * ((1 if st.nslices > 0 else 0) + (1 if st.nlong > 0 else 0))
-    res = dict(n=n, nnz=nnz, t_total=t_total, per_launch=per_launch, clocks=clocks, e2e=e2e, launches=launches,
-               stats=st, ctx=ctx, cplx=cplx)
+               "d2h_bytes_per_step": d2h, "call": "mpsg_spmv_complex" if cplx else "mpsg_spmv"}
+    if local_stats is not None:
+        kernels = (1 if local_stats.nslices > 0 else 0) + (1 if local_stats.nlong > 0 else 0)
+    else:
+        kernels = 2  # upper bound for a shard (SELL + long-row kernel)
+    res = dict(n=n, nnz=nnz, units=units, t_total=t_total, per_launch=t_total / args.steps, clocks=clocks,
+               e2e=e2e, launches=args.steps * kernels, cplx=cplx, halo_rows=halo, shard=shard)
+    del dA
+    if comm:
+        comm.close()
+    ctx.close()
     return res
+
+
+def run_gpu_cg(args, K, order, rank, world, dist):
+    """Config 5: 500 CG iterations (fixed budget, rel_tol 1e-30 so none stops early)."""
+    import torch
+
+    import paper_2412_17510_b200 as M
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream, ctx = setup_stream(torch, M, dev)
+    A, xt = make_inputs("cfg5", K)
+    n, nnz = A.nrows, A.nnz
+    shard = args.shard and world > 1
+    cfg = M.SolverConfig(rel_tol=1e-30, max_iters=CG_ITERS, lanes_enabled=order != 0, fast=order == 2)
+    comm = None
+    if shard:
+        comm = make_comm(M, ctx, world, rank, dist)
+        dA = M.DistCsr.from_global(comm, A, K)
+        b0, e0 = dA.row_begin, dA.row_end
+        bfull = M.spmv(M.DeviceCsr(A, K, ctx=ctx), xt, M.ORDER_LANE4)
+        b = np.ascontiguousarray(bfull[b0:e0])
+        solve = lambda: M.dsolve_cg(dA, b, cfg)  # noqa: E731
+        units = nnz * CG_ITERS
+    else:
+        dA = M.DeviceCsr(A, K, ctx=ctx)
+        b = M.spmv(dA, xt, M.ORDER_LANE4)
+        op = M.CsrOperator(dA)
+        solve = lambda: M.solve_cg(op, b, cfg)  # noqa: E731
+        units = world * nnz * CG_ITERS
+    for _ in range(max(1, args.warmup // 3)):
+        solve()
+    clk = ClockSampler(dev.index)
+    clk.start()
+    if dist:
+        dist.barrier()
+    loop, wall, res = [], [], None
+    for _ in range(max(1, args.steps // 5)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = solve()
+        wall.append(time.perf_counter() - t0)
+        loop.append(res.report.device_seconds)
+    if dist:
+        dist.barrier()
+    clocks = clk.stop()
+    t_loop = max_over_ranks(torch, dev, dist, statistics.median(loop))
+    t_wall = max_over_ranks(torch, dev, dist, statistics.median(wall))
+    rep = res.report
+    out = dict(n=n, nnz=nnz, units=units, t_total=t_loop, per_iter=t_loop / CG_ITERS, clocks=clocks,
+               e2e={"value": units / t_wall / 1e9, "unit": "Gnnz/s (CG SpMV work)",
+                    "h2d_bytes_per_step": int(b.nbytes), "d2h_bytes_per_step": int(b.nbytes) + 8 * (CG_ITERS + 1),
+                    "call": "mpsg_dcg" if shard else "mpsg_cg"},
+               iterations=rep.iterations, rel_residual=rep.residual_history[-1] / rep.residual_history[0],
+               true_residual=rep.final_true_residual, shard=shard, cplx=False, halo_rows=0,
+               launches=CG_ITERS * 5)
+    del dA
+    if comm:
+        comm.close()
+    ctx.close()
+    return out
+
+
+def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey):
+    if kind == "cg":
+        byts, ops = cg_iter_bytes(nnz, n, K), cg_iter_ops(nnz, n, K)
+    else:
+        byts, ops = algorithmic_bytes(nnz, n, K, cplx), algorithmic_ops(nnz, K, cplx)
+    t_hbm, t_fp = byts / (hbm_peak * 1e9), ops / fp64_peak
+    if t_hbm >= t_fp:
+        ach = byts / seconds / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        ach = ops / seconds / 1e12
+        pk = fp64_peak / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": pk, "unit": "T fp64 instr/s", "frac": ach / pk,
+                "peak_source": "measured on this GPU by mpsg_measure_fp64_peak (DFMA throughput)"}
+    roof.update(t_roofline_us=max(t_hbm, t_fp) * 1e6, algorithmic_bytes=byts, algorithmic_fp64_ops=ops,
+                per=("one CG iteration" if kind == "cg" else "one SpMV launch"),
+                traffic=traffic_for(tkey))
+    return roof
 
 
 def main():
@@ -288,12 +439,16 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--K", type=int, default=4)
     ap.add_argument("--order", default="fast", choices=["fast", "lane4", "scalar"])
+    ap.add_argument("--shard", action="store_true", help="row-shard the matrix across ranks (configs 3, 4, 5)")
+    ap.add_argument("--cg", action="store_true", help="config 5: 500-iteration CG instead of one SpMV")
     ap.add_argument("--all", action="store_true", help="one line per config/precision (not the driver line)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--secondary", default="", help="extra K to report beside the headline (default: TD for cfg2)")
+    ap.add_argument("--secondary", default="", help="'none' disables the TD line beside the cfg2 QD headline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.cg:
+        args.config = "cfg5"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -303,12 +458,13 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        r = run_reference(args, args.config, args.K)
+        r = run_reference(args.steps, args.warmup, args.config, args.K, cg=args.cg)
         line = {"metric": METRIC, "value": r["value"], "unit": "Gnnz/s", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": r["median_s"] * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "impl": "reference",
-                "config": {"workload": f"{args.config} {K_NAME[args.K]}: {CONFIG_DESC[args.config]}",
+                "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded generators, synth/mpsgen.c)", "impl": "reference",
+                "config": {"workload": f"{args.config} {K_NAME[args.K]}{' CG' if args.cg else ''}: "
+                                       f"{CONFIG_DESC[args.config]}",
                            "precision": K_NAME[args.K], "order": "lane4 (reference default)"},
                 "cpu_baseline": {"value": r["value"], "unit": "Gnnz/s", "cores": r["cores"], "kind": r["kind"],
                                  "sample": r["sample"]},
@@ -323,89 +479,78 @@ def main():
         import torch.distributed as tdist
 
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl")
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
     else:
         torch.cuda.set_device(0)
 
     import paper_2412_17510_b200 as M
 
-    hbm_peak, hbm_src = measured_peaks()
+    hbm_peak, _ = measured_peaks()
     probe = M.Context(torch.cuda.current_device())
     fp64_peak = M.measure_fp64_peak(probe)
     probe.close()
 
-    jobs = [(args.config, args.K)]
+    jobs = [(args.config, args.K, args.cg)]
     if args.all:
-        jobs = [("cfg1", 2), ("cfg2", 3), ("cfg2", 4), ("cfg3", 2), ("cfg3", 4), ("cfg4", 2), ("cfg5", 2), ("cfg5", 4)]
+        jobs = [("cfg1", 2, False), ("cfg2", 3, False), ("cfg2", 4, False), ("cfg3", 2, False), ("cfg3", 4, False),
+                ("cfg4", 2, False), ("cfg5", 2, False), ("cfg5", 4, False), ("cfg5", 2, True), ("cfg5", 4, True)]
     secondary = None
-    if not args.all and args.config == "cfg2" and args.K == 4 and args.secondary != "none":
-        secondary = ("cfg2", 3)
-
-    def describe(cfg, K, r):
-        cplx = r["cplx"]
-        nnz, n = r["nnz"], r["n"]
-        byts = algorithmic_bytes(nnz, n, K, cplx)
-        ops = algorithmic_ops(nnz, K, cplx)
-        t_hbm, t_fp = byts / (hbm_peak * 1e9), ops / fp64_peak
-        bound = "hbm" if t_hbm >= t_fp else "fp64"
-        if bound == "hbm":
-            ach = byts / r["per_launch"] / 1e9
-            roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                    "peak_source": hbm_src}
-        else:
-            ach = ops / r["per_launch"] / 1e12
-            pk = fp64_peak / 1e12
-            roof = {"bound": "fp64", "achieved": ach, "peak": pk, "unit": "Tops/s (fp64 instr)", "frac": ach / pk,
-                    "peak_source": "measured on this GPU by mpsg_measure_fp64_peak (DFMA throughput)"}
-        roof["t_roofline_us"] = max(t_hbm, t_fp) * 1e6
-        roof["algorithmic_bytes"] = byts
-        roof["algorithmic_fp64_ops"] = ops
-        roof["traffic"] = traffic_for(cfg, K)
-        return roof
+    if not args.all and args.config == "cfg2" and args.K == 4 and not args.cg and args.secondary != "none":
+        secondary = ("cfg2", 3, False)
 
     results = []
-    for cfg, K in jobs + ([secondary] if secondary else []):
-        r = run_gpu(args, cfg, K, order, rank, world, dist)
-        r["roof"] = describe(cfg, K, r)
-        results.append((cfg, K, r))
-        r["ctx"].close()
+    for cfg, K, cg in jobs + ([secondary] if secondary else []):
+        if cg:
+            r = run_gpu_cg(args, K, order, rank, world, dist)
+            r["roof"] = roofline("cg", r["nnz"], r["n"], K, False, r["per_iter"], hbm_peak, fp64_peak,
+                                 f"cg5_K{K}")
+        else:
+            r = run_gpu_spmv(args, cfg, K, order, rank, world, dist)
+            r["roof"] = roofline("spmv", r["nnz"], r["n"], K, r["cplx"], r["per_launch"], hbm_peak, fp64_peak,
+                                 f"{cfg}_K{K}")
+        results.append((cfg, K, cg, r))
 
     if rank == 0:
-        for idx, (cfg, K, r) in enumerate(results[: len(jobs)]):
-            value = world * r["nnz"] * args.steps / r["t_total"] / 1e9
+        for idx, (cfg, K, cg, r) in enumerate(results[: len(jobs)]):
+            steps = 1 if cg else args.steps
+            value = r["units"] * steps / r["t_total"] / 1e9
+            if r["shard"]:
+                par = f"row-sharded x{world} (equal-nnz blocks, NCCL x halo)"
+            else:
+                par = f"replicas x{world}" if world > 1 else "single GPU"
             line = {"metric": METRIC, "value": value, "unit": "Gnnz/s", "n_gpus": world, "steps": args.steps,
-                    "warmup": args.warmup, "ms_per_step": r["t_total"] / args.steps * 1e3,
-                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                    "warmup": args.warmup,
+                    "ms_per_step": (r["t_total"] * 1e3 if cg else r["t_total"] / args.steps * 1e3),
+                    "higher_is_better": True, "scaling": "strong" if r["shard"] else "weak",
+                    "vs_baseline": None, "dtype": "f64",
                     "data": "synthetic (seeded generators, synth/mpsgen.c)",
-                    "config": {"workload": f"{cfg} {K_NAME[K]}: {CONFIG_DESC[cfg]}", "precision": K_NAME[K],
-                               "order": args.order, "nnz": r["nnz"], "n": r["n"],
-                               "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                               "l2": "flushed before every timed step: 256 MB write, then 256 MB read of a second buffer"},
+                    "config": {"workload": f"{cfg} {K_NAME[K]}{' CG x500' if cg else ''}: {CONFIG_DESC[cfg]}",
+                               "precision": K_NAME[K], "order": args.order, "nnz": r["nnz"], "n": r["n"],
+                               "parallelism": par,
+                               "l2": ("flushed before every timed step: 256 MB write, then 256 MB read of a "
+                                      "second buffer") if not cg else "inputs (A, vectors) larger than L2"},
                     "roofline": r["roof"], "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["launches"]}
+            if cg:
+                line["config"].update(step="one 500-iteration CG solve (graph-captured batches of 32)",
+                                      iterations=r["iterations"], rel_residual=r["rel_residual"],
+                                      true_residual=r["true_residual"])
+                line["ms_per_iteration"] = r["per_iter"] * 1e3
+            if r["shard"]:
+                line["config"]["halo_rows_rank0"] = r["halo_rows"]
             if secondary and idx == 0:
-                c2, k2, r2 = results[-1]
+                c2, k2, _, r2 = results[-1]
                 line["secondary"] = {"workload": f"{c2} {K_NAME[k2]}",
-                                     "value": world * r2["nnz"] * args.steps / r2["t_total"] / 1e9,
-                                     "unit": "Gnnz/s", "roofline": r2["roof"],
-                                     "e2e": r2["e2e"]}
+                                     "value": r2["units"] * args.steps / r2["t_total"] / 1e9,
+                                     "unit": "Gnnz/s", "roofline": r2["roof"], "e2e": r2["e2e"]}
             if world == 1 and not args.no_cpu and not args.all:
-                cb = run_reference(argparse.Namespace(steps=5, warmup=1), cfg, K)
+                cb = run_reference(5 if not cg else 1, 1 if not cg else 0, cfg, K, cg=cg)
                 line["cpu_baseline"] = {"value": cb["value"], "unit": "Gnnz/s", "cores": cb["cores"],
                                         "kind": cb["kind"], "sample": cb["sample"]}
             print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
-
-
-def traffic_for(cfg, K):
-    p = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d.get(f"{cfg}_K{K}")
-    return None
 
 
 if __name__ == "__main__":

@@ -119,8 +119,9 @@ typedef struct mpsg_cg_report {
   double final_recurrence_residual;
   double final_true_residual;
   double setup_seconds;
-  double solve_seconds;
+  double solve_seconds;   /* host wall clock of the iteration loop (as the reference) */
   char detail[64];
+  double device_seconds;  /* the same loop timed with CUDA events on the solve stream */
 } mpsg_cg_report;
 
 /* ---- context --------------------------------------------------------- */

@@ -66,7 +66,7 @@ class _CgReport(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("converged", ctypes.c_int32), ("iterations", _i64),
                 ("history_len", _i64), ("rhs_norm", _f64), ("final_recurrence_residual", _f64),
                 ("final_true_residual", _f64), ("setup_seconds", _f64), ("solve_seconds", _f64),
-                ("detail", ctypes.c_char * 64)]
+                ("detail", ctypes.c_char * 64), ("device_seconds", _f64)]
 
 
 _lib = None
@@ -336,6 +336,7 @@ class SolverReport:  # krylov.hpp:77-88
     final_true_residual: float = 0.0
     setup_seconds: float = 0.0
     solve_seconds: float = 0.0
+    device_seconds: float = 0.0  # iteration loop timed with CUDA events (not in the reference)
 
 
 @dataclass
@@ -395,7 +396,7 @@ def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult
         iterations=int(rep.iterations), residual_history=hist[: rep.history_len].tolist(),
         rhs_norm=rep.rhs_norm, final_recurrence_residual=rep.final_recurrence_residual,
         final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
-        solve_seconds=rep.solve_seconds)
+        solve_seconds=rep.solve_seconds, device_seconds=rep.device_seconds)
     return SolveResult(x, report)
 
 
@@ -535,7 +536,7 @@ def dsolve_cg(A: DistCsr, b_local, cfg: SolverConfig | None = None) -> SolveResu
         iterations=int(rep.iterations), residual_history=hist[: rep.history_len].tolist(),
         rhs_norm=rep.rhs_norm, final_recurrence_residual=rep.final_recurrence_residual,
         final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
-        solve_seconds=rep.solve_seconds)
+        solve_seconds=rep.solve_seconds, device_seconds=rep.device_seconds)
     return SolveResult(x, report)
 
 

@@ -146,6 +146,10 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
     status = hs;
   }
   int gbatch = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  CG_TRY(cudaEventCreate(&ev0));
+  CG_TRY(cudaEventCreate(&ev1));
+  CG_TRY(cudaEventRecord(ev0, st));
   while (status == CG_RUNNING) {
     long long remaining = max_iters - done_k;
     int nb = (int)std::min<long long>(batch, remaining);
@@ -177,9 +181,15 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
     CG_TRY(cudaStreamSynchronize(st));
     status = hs;
   }
+  CG_TRY(cudaEventRecord(ev1, st));
   CgState<K> hst;
   CG_TRY(cudaMemcpy(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost));
   const double t_solve = now_s();
+  float dev_ms = 0.f;
+  cudaEventSynchronize(ev1);
+  cudaEventElapsedTime(&dev_ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
   // Iteration count semantics (krylov.hpp:251-253, 262-268, 276).
   const int64_t iters = hst.k;
   const int fstatus = hst.status == CG_RUNNING ? MPSG_MAX_ITERATIONS : hst.status;
@@ -209,6 +219,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   rep->final_true_residual = true_res;
   rep->setup_seconds = t_setup - t0;
   rep->solve_seconds = t_solve - t_setup;
+  rep->device_seconds = dev_ms * 1e-3;
   const char* detail = "";
   if (fstatus == MPSG_BREAKDOWN) detail = hst.reason == 1 ? "cg: <p, Ap> vanished" : "cg: non-finite residual";
   std::snprintf(rep->detail, sizeof(rep->detail), "%s", detail);

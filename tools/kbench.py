@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("specs", nargs="+")
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--tag", default=os.environ.get("MPSG_LIB", "default"))
     ap.add_argument("--check", action="store_true", help="compare with the LANE4 checksum goldens")
     args = ap.parse_args()
@@ -60,7 +61,7 @@ def main():
             dx = torch.from_numpy(x).to(dev)
             dy = torch.empty((n, K), dtype=torch.float64, device=dev)
             step = lambda: M.spmv_dev(dA, dx.data_ptr(), dy.data_ptr(), order, stream.cuda_stream)  # noqa
-        for _ in range(3):
+        for _ in range(args.warmup):
             step()
         ms = []
         for _ in range(args.steps):
