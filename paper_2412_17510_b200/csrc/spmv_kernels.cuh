@@ -84,9 +84,20 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
     MC<K> L[P];
 #pragma unroll
     for (int c = 0; c < P; ++c) L[c] = zero<K>();
-    for (int m = 0; m < nfull; ++m) {
+    if constexpr (P == 1 && K > 2) {
+      // one chain: the next element's column index is loaded a round ahead
+      int c = nfull > 0 ? __ldcs(cp + (int64_t)j0 * 32) : 0;
+      for (int m = 0; m < nfull; ++m) {
+        const int e = 4 * m + j0;
+        const int cn = (m + 1 < nfull) ? __ldcs(cp + (int64_t)(e + 4) * 32) : 0;
+        L[0] = add(L[0], mul(load_planes_stream<K>(vp, st, (int64_t)e * 32), load_aos<K>(x, c)));
+        c = cn;
+      }
+    } else {
+      for (int m = 0; m < nfull; ++m) {
 #pragma unroll
-      for (int c = 0; c < P; ++c) L[c] = add(L[c], sell_term<K>(vp, cp, st, x, 4 * m + j0 + c));
+        for (int c = 0; c < P; ++c) L[c] = add(L[c], sell_term<K>(vp, cp, st, x, 4 * m + j0 + c));
+      }
     }
 #pragma unroll
     for (int c = 0; c < P; ++c) s = add(s, L[c]);
@@ -150,6 +161,51 @@ MPSG_DI MC<K> chunked_row(const double* __restrict__ vp, const int* __restrict__
   return s;
 }
 
+// Lanes-off order (row_sum_scalar, kernels.hpp:90-99): one serial chain.  The
+// products of G consecutive elements are formed first (G gathers in flight),
+// then added in order.  PF = 1 also loads the next group's column indices
+// one round ahead, so its gathers can issue as soon as the group starts.
+#ifndef MPSG_SCALAR_G
+#define MPSG_SCALAR_G 2
+#endif
+#ifndef MPSG_SCALAR_PF
+#define MPSG_SCALAR_PF 1
+#endif
+template <int K, int G, int PF>
+MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
+                         const double* __restrict__ x, int len) {
+  MC<K> acc = zero<K>();
+  int k = 0;
+  if constexpr (PF) {
+    int c[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) c[j] = (j < len) ? __ldcs(cp + (int64_t)j * 32) : 0;
+    for (; k + G <= len; k += G) {
+      int cn[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) cn[j] = (k + G + j < len) ? __ldcs(cp + (int64_t)(k + G + j) * 32) : 0;
+      MC<K> p[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        p[j] = mul(load_planes_stream<K>(vp, st, (int64_t)(k + j) * 32), load_aos<K>(x, c[j]));
+#pragma unroll
+      for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
+#pragma unroll
+      for (int j = 0; j < G; ++j) c[j] = cn[j];
+    }
+  } else {
+    for (; k + G <= len; k += G) {
+      MC<K> p[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) p[j] = sell_term<K>(vp, cp, st, x, k + j);
+#pragma unroll
+      for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
+    }
+  }
+  for (; k < len; ++k) acc = add(acc, sell_term<K>(vp, cp, st, x, k));
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // SELL slice, real: one warp per slice of 32 rows, one thread per row.
 // ---------------------------------------------------------------------------
@@ -170,16 +226,7 @@ MPSG_DI void sell_real_body(const SellView& S, const double* __restrict__ x, dou
   if constexpr (K == 2 && MPSG_DD_CHUNK > 0) {
     acc = chunked_row<K, ORDER, MPSG_DD_CHUNK>(vp, cp, st, x, len);
   } else if constexpr (ORDER == ORDER_SCALAR) {
-    acc = zero<K>();
-    int k = 0;
-    for (; k + 4 <= len; k += 4) {
-      MC<K> p[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) p[j] = sell_term<K>(vp, cp, st, x, k + j);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc = add(acc, p[j]);
-    }
-    for (; k < len; ++k) acc = add(acc, sell_term<K>(vp, cp, st, x, k));
+    acc = scalar_row<K, (K == 2 ? 4 : MPSG_SCALAR_G), (K == 2 ? 0 : MPSG_SCALAR_PF)>(vp, cp, st, x, len);
   } else {
     acc = lane4_row<K, MPSG_SELL_PAR(K)>(vp, cp, st, x, len);
   }
@@ -227,14 +274,16 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
 
   MC<K> s1 = zero<K>(), s2 = zero<K>();
   if constexpr (ORDER == ORDER_SCALAR) {
+    int c = len > 0 ? __ldcs(cp) : 0;  // column index loaded a round ahead
     for (int k = 0; k < len; ++k) {
       const int64_t e = (int64_t)k * 16;
+      const int cn = (k + 1 < len) ? __ldcs(cp + e + 16) : 0;
       MC<K> a = load_planes_stream<K>(vp, st, e);
-      const int c = __ldcs(cp + e);
       MC<K> p1 = mul(a, load_aos<K>(x1, c));
       MC<K> p2 = mul(a, load_aos<K>(x2, c));
       s1 = add(s1, p1);
       s2 = add(s2, p2);
+      c = cn;
     }
   } else {
     // the two sums' lane chains one at a time (reference order, fewer live
