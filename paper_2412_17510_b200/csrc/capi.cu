@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -87,9 +88,10 @@ __global__ void build_long_kernel(const int* lrow, const int64_t* lptr, const in
 
 void free_csr(mpsg_csr* A) {
   if (!A) return;
-  void* ptrs[] = {A->slice_ptr, A->slot_row, A->slot_len, A->scol,  A->sval,
-                  A->lrow,      A->lptr,     A->lcol,     A->lval,  A->chunk_row,
-                  A->chunk_first, A->partial, A->counter};
+  void* ptrs[] = {A->slice_ptr, A->slot_row,    A->slot_len, A->scol,      A->sval,
+                  A->lrow,      A->lptr,        A->lcol,     A->lval,      A->chunk_row,
+                  A->chunk_beg, A->chunk_end,   A->chunk_slot, A->chunk_first, A->partial,
+                  A->counter};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete A;
@@ -162,6 +164,8 @@ int mpsg_ctx_create(int device, mpsg_ctx** out) {
   if (const char* s = std::getenv("MPSG_LONG_THRESHOLD")) ctx->long_threshold = std::atoll(s);
   if (const char* s = std::getenv("MPSG_SIGMA")) ctx->sigma = std::atoll(s);
   if (const char* s = std::getenv("MPSG_FAST_CHUNK")) ctx->fast_chunk = std::atoll(s);
+  if (const char* s = std::getenv("MPSG_COLBLOCK_BYTES")) ctx->colblock_bytes = std::atoll(s);
+  if (const char* s = std::getenv("MPSG_COLBLOCK_MIN")) ctx->colblock_min = std::atoll(s);
   *out = ctx;
   return MPSG_OK;
 }
@@ -293,14 +297,53 @@ int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t
   // long store plan
   A->nlong = (int64_t)long_rows.size();
   std::vector<int64_t> lptr((size_t)A->nlong + 1, 0);
-  std::vector<int> chunk_first((size_t)A->nlong + 1, 0), chunk_row;
   for (int64_t r = 0; r < A->nlong; ++r) {
     const int row = long_rows[(size_t)r];
-    const int64_t len = indptr[row + 1] - indptr[row];
-    lptr[(size_t)r + 1] = lptr[(size_t)r] + len;
-    const int64_t nch = (len + A->chunk - 1) / A->chunk;
-    chunk_first[(size_t)r + 1] = chunk_first[(size_t)r] + (int)nch;
-    for (int64_t c = 0; c < nch; ++c) chunk_row.push_back((int)r);
+    lptr[(size_t)r + 1] = lptr[(size_t)r] + (indptr[row + 1] - indptr[row]);
+  }
+  // Fast-order chunks of the long rows.  Each row is cut where its (sorted)
+  // columns cross a column-block boundary -- a block = colblock_bytes of x --
+  // and every piece into chunks of at most `chunk` elements.  Chunks are then
+  // ordered block-major, so the warps running at any one time gather from
+  // one block of x (L2-resident) instead of all of it.  Slots (the partial
+  // sums' combine order) follow row position, so the result does not depend
+  // on the blocking.
+  std::vector<int> chunk_first((size_t)A->nlong + 1, 0), chunk_row, chunk_slot;
+  std::vector<int64_t> chunk_beg, chunk_end;
+  {
+    const int64_t xb = (int64_t)K * 8 * (A->cplx ? 2 : 1);
+    const int64_t W = ctx->colblock_bytes > 0 ? std::max<int64_t>(1, ctx->colblock_bytes / xb) : ncols + 1;
+    const int64_t B = std::max<int64_t>(1, (ncols + W - 1) / W);
+    std::vector<std::vector<std::array<int64_t, 4>>> per_block((size_t)B);  // (row, beg, end, slot)
+    int slot = 0;
+    for (int64_t r = 0; r < A->nlong; ++r) {
+      const int row = long_rows[(size_t)r];
+      const int64_t src = indptr[row], len = indptr[row + 1] - src;
+      bool sorted = true;
+      if (B > 1 && len >= ctx->colblock_min)
+        for (int64_t k = 1; k < len && sorted; ++k) sorted = indices[src + k] >= indices[src + k - 1];
+      const bool split = B > 1 && len >= ctx->colblock_min && sorted;
+      int64_t k = 0;
+      while (k < len) {
+        const int64_t blk = split ? std::min<int64_t>(B - 1, indices[src + k] / W) : 0;
+        int64_t kend = len;
+        if (split && blk + 1 < B) {  // first position with column >= (blk+1)*W
+          kend = std::lower_bound(indices + src + k, indices + src + len, (blk + 1) * W) - (indices + src);
+        }
+        for (int64_t c = k; c < kend; c += A->chunk)
+          per_block[(size_t)blk].push_back({r, lptr[(size_t)r] + c, lptr[(size_t)r] + std::min(kend, c + A->chunk),
+                                            (int64_t)slot++});
+        k = kend;
+      }
+      chunk_first[(size_t)r + 1] = slot;
+    }
+    for (auto& v : per_block)
+      for (auto& c : v) {
+        chunk_row.push_back((int)c[0]);
+        chunk_beg.push_back(c[1]);
+        chunk_end.push_back(c[2]);
+        chunk_slot.push_back((int)c[3]);
+      }
   }
   A->long_nnz = lptr.back();
   A->nchunks = (int64_t)chunk_row.size();
@@ -358,12 +401,18 @@ int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t
     if ((rc = dev_alloc(ctx, A, &A->lcol, (size_t)A->long_nnz))) return rc;
     if ((rc = dev_alloc(ctx, A, &A->lval, (size_t)A->long_nnz * nplanes))) return rc;
     if ((rc = dev_alloc(ctx, A, &A->chunk_row, (size_t)A->nchunks))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->chunk_beg, (size_t)A->nchunks))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->chunk_end, (size_t)A->nchunks))) return rc;
+    if ((rc = dev_alloc(ctx, A, &A->chunk_slot, (size_t)A->nchunks))) return rc;
     if ((rc = dev_alloc(ctx, A, &A->chunk_first, (size_t)A->nlong + 1))) return rc;
     if ((rc = dev_alloc(ctx, A, &A->partial, (size_t)A->nchunks * NS * K))) return rc;
     if ((rc = dev_alloc(ctx, A, &A->counter, (size_t)A->nlong))) return rc;
     CUDA_TRY(ctx, cudaMemcpyAsync(A->lrow, long_rows.data(), long_rows.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     CUDA_TRY(ctx, cudaMemcpyAsync(A->lptr, lptr.data(), lptr.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     CUDA_TRY(ctx, cudaMemcpyAsync(A->chunk_row, chunk_row.data(), chunk_row.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->chunk_beg, chunk_beg.data(), chunk_beg.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->chunk_end, chunk_end.data(), chunk_end.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(A->chunk_slot, chunk_slot.data(), chunk_slot.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     CUDA_TRY(ctx, cudaMemcpyAsync(A->chunk_first, chunk_first.data(), chunk_first.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     CUDA_TRY(ctx, cudaMemsetAsync(A->counter, 0, (size_t)A->nlong * sizeof(unsigned), st));
     build_long_kernel<<<(unsigned)A->nlong, 256, 0, st>>>(A->lrow, A->lptr, d_indptr, d_indices, d_planes,

@@ -31,6 +31,11 @@ struct mpsg_ctx {
   int64_t long_threshold = 256;
   int64_t sigma = 16384;
   int64_t fast_chunk = 2048;
+  // column blocking of long-row chunks (fast order): rows of at least
+  // colblock_min elements are cut where their columns cross a multiple of
+  // colblock_bytes worth of x; 0 disables.
+  int64_t colblock_bytes = 16ll << 20;
+  int64_t colblock_min = 4096;
 };
 
 struct mpsg_csr {
@@ -52,6 +57,9 @@ struct mpsg_csr {
   int* lcol = nullptr;
   double* lval = nullptr;
   int* chunk_row = nullptr;
+  int64_t* chunk_beg = nullptr;
+  int64_t* chunk_end = nullptr;
+  int* chunk_slot = nullptr;
   int* chunk_first = nullptr;
   double* partial = nullptr;
   unsigned* counter = nullptr;
@@ -62,7 +70,7 @@ struct mpsg_csr {
   }
   LongView lng() const {
     return LongView{(int)nlong, lrow, lptr, lcol, lval, long_nnz, (int)chunk, (int)nchunks,
-                    chunk_row, chunk_first, partial, counter};
+                    chunk_row, chunk_beg, chunk_end, chunk_slot, chunk_first, partial, counter};
   }
 };
 

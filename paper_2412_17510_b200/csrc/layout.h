@@ -41,11 +41,18 @@ struct LongView {
   const int* col;            // [lnnz]
   const double* val;         // [nplanes][lnnz]
   int64_t stride;            // lnnz
-  // fast-mode chunking (warp per chunk of `chunk` elements)
+  // fast-mode chunking: warp w sums elements [chunk_beg[w], chunk_end[w]) of
+  // long row chunk_row[w] into partial slot chunk_slot[w]; the slots of a row
+  // are [chunk_first[r], chunk_first[r+1]) in row-position order.  Chunks are
+  // ordered column-block-major (see capi.cu) so concurrently running warps
+  // gather from one block of x at a time.
   int chunk;
   int nchunks;
   const int* chunk_row;      // [nchunks] long-row index
-  const int* chunk_first;    // [nrows+1] first chunk of each long row
+  const int64_t* chunk_beg;  // [nchunks] offsets into col/val
+  const int64_t* chunk_end;  // [nchunks]
+  const int* chunk_slot;     // [nchunks] partial slot
+  const int* chunk_first;    // [nrows+1] first slot of each long row
   double* partial;           // [nchunks][nsum*K]
   unsigned* counter;         // [nrows] arrival counters (self-resetting)
 };

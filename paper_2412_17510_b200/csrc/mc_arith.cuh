@@ -399,10 +399,77 @@ MPSG_DI bool less_equal(const MC<K>& x, const MC<K>& y) {  // multicomp.hpp:390-
 }
 
 // -------------------------------------------------------- memory helpers --
+// L2 eviction-priority hints (createpolicy + ld.global.L2::cache_hint): the
+// gathered vector x is loaded evict_last so the streamed matrix (evict_first)
+// does not push it out of L2.  MPSG_X_HINT / MPSG_A_HINT select them.
+#ifndef MPSG_X_HINT
+#define MPSG_X_HINT 0
+#endif
+#ifndef MPSG_A_HINT
+#define MPSG_A_HINT 0
+#endif
+MPSG_DI uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+MPSG_DI uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+MPSG_DI double2 ld_v2_hint(const double* q, uint64_t pol) {
+  double2 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(q), "l"(pol));
+  return r;
+}
+MPSG_DI double ld_f64_hint(const double* q, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(q), "l"(pol));
+  return r;
+}
+MPSG_DI double ld_f64_stream(const double* q) {
+#if MPSG_A_HINT
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(r)
+               : "l"(q), "l"(policy_evict_first()));
+  return r;
+#else
+  return __ldcs(q);
+#endif
+}
+MPSG_DI int ld_s32_stream(const int* q) {
+#if MPSG_A_HINT
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(r)
+               : "l"(q), "l"(policy_evict_first()));
+  return r;
+#else
+  return __ldcs(q);
+#endif
+}
+
 template <int K>
 MPSG_DI MC<K> load_aos(const double* __restrict__ p, int64_t i) {
   MC<K> r;
   const double* q = p + i * K;
+#if MPSG_X_HINT
+  const uint64_t pol = policy_evict_last();
+  if constexpr (K == 2 || K == 4) {
+#pragma unroll
+    for (int h = 0; h < K / 2; ++h) {
+      double2 v = ld_v2_hint(q + 2 * h, pol);
+      r.c[2 * h] = v.x;
+      r.c[2 * h + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) r.c[j] = ld_f64_hint(q + j, pol);
+  }
+  return r;
+#endif
   if constexpr (K == 2) {
     double2 v = __ldg(reinterpret_cast<const double2*>(q));
     r.c[0] = v.x;

@@ -39,7 +39,7 @@ template <int K>
 MPSG_DI MC<K> load_planes_stream(const double* __restrict__ val, int64_t stride, int64_t e) {
   MC<K> a;
 #pragma unroll
-  for (int j = 0; j < K; ++j) a.c[j] = __ldcs(val + j * stride + e);
+  for (int j = 0; j < K; ++j) a.c[j] = ld_f64_stream(val + j * stride + e);
   return a;
 }
 
@@ -65,7 +65,7 @@ template <int K>
 MPSG_DI MC<K> sell_term(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
                         const double* __restrict__ x, int k) {
   const int64_t e = (int64_t)k * 32;
-  return mul(load_planes_stream<K>(vp, st, e), load_aos<K>(x, __ldcs(cp + e)));
+  return mul(load_planes_stream<K>(vp, st, e), load_aos<K>(x, ld_s32_stream(cp + e)));
 }
 
 // LANE4 order with the four lane chains evaluated P at a time.  Chain j
@@ -86,10 +86,10 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
     for (int c = 0; c < P; ++c) L[c] = zero<K>();
     if constexpr (P == 1 && K > 2) {
       // one chain: the next element's column index is loaded a round ahead
-      int c = nfull > 0 ? __ldcs(cp + (int64_t)j0 * 32) : 0;
+      int c = nfull > 0 ? ld_s32_stream(cp + (int64_t)j0 * 32) : 0;
       for (int m = 0; m < nfull; ++m) {
         const int e = 4 * m + j0;
-        const int cn = (m + 1 < nfull) ? __ldcs(cp + (int64_t)(e + 4) * 32) : 0;
+        const int cn = (m + 1 < nfull) ? ld_s32_stream(cp + (int64_t)(e + 4) * 32) : 0;
         L[0] = add(L[0], mul(load_planes_stream<K>(vp, st, (int64_t)e * 32), load_aos<K>(x, c)));
         c = cn;
       }
@@ -128,7 +128,7 @@ MPSG_DI MC<K> chunked_row(const double* __restrict__ vp, const int* __restrict__
   auto load_chunk = [&](int k0, int lim, MC<K>* p) {
     int c[CH];
 #pragma unroll
-    for (int i = 0; i < CH; ++i) c[i] = __ldcs(cp + (int64_t)min(k0 + i, lim - 1) * 32);
+    for (int i = 0; i < CH; ++i) c[i] = ld_s32_stream(cp + (int64_t)min(k0 + i, lim - 1) * 32);
     MC<K> xv[CH];
 #pragma unroll
     for (int i = 0; i < CH; ++i) xv[i] = load_aos<K>(x, c[i]);
@@ -179,11 +179,11 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
   if constexpr (PF) {
     int c[G];
 #pragma unroll
-    for (int j = 0; j < G; ++j) c[j] = (j < len) ? __ldcs(cp + (int64_t)j * 32) : 0;
+    for (int j = 0; j < G; ++j) c[j] = (j < len) ? ld_s32_stream(cp + (int64_t)j * 32) : 0;
     for (; k + G <= len; k += G) {
       int cn[G];
 #pragma unroll
-      for (int j = 0; j < G; ++j) cn[j] = (k + G + j < len) ? __ldcs(cp + (int64_t)(k + G + j) * 32) : 0;
+      for (int j = 0; j < G; ++j) cn[j] = (k + G + j < len) ? ld_s32_stream(cp + (int64_t)(k + G + j) * 32) : 0;
       MC<K> p[G];
 #pragma unroll
       for (int j = 0; j < G; ++j)
@@ -274,10 +274,10 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
 
   MC<K> s1 = zero<K>(), s2 = zero<K>();
   if constexpr (ORDER == ORDER_SCALAR) {
-    int c = len > 0 ? __ldcs(cp) : 0;  // column index loaded a round ahead
+    int c = len > 0 ? ld_s32_stream(cp) : 0;  // column index loaded a round ahead
     for (int k = 0; k < len; ++k) {
       const int64_t e = (int64_t)k * 16;
-      const int cn = (k + 1 < len) ? __ldcs(cp + e + 16) : 0;
+      const int cn = (k + 1 < len) ? ld_s32_stream(cp + e + 16) : 0;
       MC<K> a = load_planes_stream<K>(vp, st, e);
       MC<K> p1 = mul(a, load_aos<K>(x1, c));
       MC<K> p2 = mul(a, load_aos<K>(x2, c));
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
       for (int m = 0; m < nfull; ++m) {
         const int64_t e = (int64_t)(4 * m + j) * 16;
         MC<K> a = load_planes_stream<K>(vp, st, e);
-        const int c = __ldcs(cp + e);
+        const int c = ld_s32_stream(cp + e);
         L1 = add(L1, mul(a, load_aos<K>(x1, c)));
         L2 = add(L2, mul(a, load_aos<K>(x2, c)));
       }
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
     for (int k = nfull * 4; k < len; ++k) {
       const int64_t e = (int64_t)k * 16;
       MC<K> a = load_planes_stream<K>(vp, st, e);
-      const int c = __ldcs(cp + e);
+      const int c = ld_s32_stream(cp + e);
       s1 = add(s1, mul(a, load_aos<K>(x1, c)));
       s2 = add(s2, mul(a, load_aos<K>(x2, c)));
     }
@@ -402,8 +402,13 @@ __global__ void __launch_bounds__(128) long_det_kernel(LongView L, const double*
 // elements (coalesced), a fixed xor-tree reduces the warp, and the last
 // arriving warp of a row adds the chunk partials in chunk order.
 // ---------------------------------------------------------------------------
+#ifdef MPSG_LONG_MINB
+#define MPSG_LONG_LB __launch_bounds__(128, MPSG_LONG_MINB)
+#else
+#define MPSG_LONG_LB __launch_bounds__(128)
+#endif
 template <int K, bool CPLX>
-__global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double* __restrict__ xre,
+__global__ void MPSG_LONG_LB long_fast_kernel(LongView L, const double* __restrict__ xre,
                                                         const double* __restrict__ xim,
                                                         double* __restrict__ yre,
                                                         double* __restrict__ yim) {
@@ -414,15 +419,14 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
   const int r = L.chunk_row[w];
   const int first = L.chunk_first[r];
   const int nch = L.chunk_first[r + 1] - first;
-  const int64_t rb = L.ptr[r], re = L.ptr[r + 1];
-  const int64_t b = rb + (int64_t)(w - first) * L.chunk;
-  const int64_t e = (b + L.chunk < re) ? b + L.chunk : re;
+  const int64_t b = L.chunk_beg[w];
+  const int64_t e = L.chunk_end[w];
 
   // U independent partial sums per lane (element k goes to partial
   // ((k - b) / 32) % U), so U gathers are in flight per thread; combined in
   // fixed order below.
 #ifndef MPSG_LONG_U
-#define MPSG_LONG_U 2
+#define MPSG_LONG_U 1
 #endif
   constexpr int U = CPLX ? 1 : MPSG_LONG_U;
   MC<K> acc[NS];
@@ -432,15 +436,28 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #pragma unroll
     for (int s = 0; s < NS; ++s) pu[u][s] = zero<K>();
   int64_t k = b + lane;
+  // column indices are loaded one round ahead (real case), so a round's
+  // gathers issue as soon as it starts
+  int cpf[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) cpf[u] = (!CPLX && k + 32 * u < e) ? ld_s32_stream(L.col + k + 32 * u) : 0;
   for (; k + 32 * (U - 1) < e; k += 32 * U) {
+    int cnx[U];
+    if constexpr (!CPLX) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t kn = k + 32 * (U + u);
+        cnx[u] = kn < e ? ld_s32_stream(L.col + kn) : 0;
+      }
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t kk = k + 32 * u;
-      const int c = __ldcs(L.col + kk);
       MC<K> are = load_planes_stream<K>(L.val, L.stride, kk);
       if constexpr (!CPLX) {
-        pu[u][0] = add(pu[u][0], mul(are, load_aos<K>(xre, c)));
+        pu[u][0] = add(pu[u][0], mul(are, load_aos<K>(xre, cpf[u])));
       } else {
+        const int c = ld_s32_stream(L.col + kk);
         MC<K> aim = load_planes_stream<K>(L.val + (int64_t)K * L.stride, L.stride, kk);
         MC<K> vr = load_aos<K>(xre, c), vi = load_aos<K>(xim, c);
         pu[u][0] = add(pu[u][0], mul(are, vr));
@@ -449,14 +466,17 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
         pu[u][3] = add(pu[u][3], mul(aim, vr));
       }
     }
+    if constexpr (!CPLX) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) cpf[u] = cnx[u];
+    }
   }
 #pragma unroll
   for (int u = 0; u < U - 1; ++u) {  // remainder: at most U-1 more elements per lane
     const int64_t kk = k + 32 * u;
     if (kk < e) {
-      const int c = __ldcs(L.col + kk);
       MC<K> are = load_planes_stream<K>(L.val, L.stride, kk);
-      pu[u][0] = add(pu[u][0], mul(are, load_aos<K>(xre, c)));
+      pu[u][0] = add(pu[u][0], mul(are, load_aos<K>(xre, cpf[u])));
     }
   }
 #pragma unroll
@@ -483,7 +503,7 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
     if (lane == 0) finish(acc);
     return;
   }
-  double* part = L.partial + (int64_t)w * NS * K;
+  double* part = L.partial + (int64_t)L.chunk_slot[w] * NS * K;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s)
