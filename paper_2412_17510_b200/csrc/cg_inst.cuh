@@ -9,6 +9,7 @@
 #pragma once
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "cg_kernels.cuh"
@@ -32,7 +33,17 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   const int P = D ? D->comm->nranks : 1;
   const size_t vb = (size_t)n * K * sizeof(double);
   cudaStream_t st = ctx->stream;
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(DOT_MAX_BLOCKS, (n + 2047) / 2048));
+  // reduction grids: one resident wave (SMs x occupancy of the heaviest kernel)
+  int sms = 148, occ = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cg_reduce_kernel<K, 1>, DOT_THREADS, 0);
+  const char* genv = std::getenv("MPSG_CG_GRID");
+  const int gpol = genv ? std::atoi(genv) : 1;
+  const int64_t gwave = (int64_t)sms * std::max(occ, 1) * (gpol >= 2 ? gpol : 1);
+  const int G = (int)std::max<int64_t>(
+      1, std::min<int64_t>({(int64_t)DOT_MAX_BLOCKS, gpol == 0 ? (n + 2047) / 2048 : gwave,
+                            (n + DOT_THREADS - 1) / DOT_THREADS}));
+  cudaGetLastError();
   double *b = nullptr, *x = nullptr, *r = nullptr, *pfull = nullptr, *q = nullptr, *part = nullptr,
          *hist = nullptr, *loc = nullptr, *gath = nullptr;
   CgState<K>* dst = nullptr;
@@ -131,7 +142,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   const int batch = cfg->check_every > 0 ? cfg->check_every : 32;
   const int ub = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
   auto enqueue_iter = [&]() -> int {
-    int e = apply(q);
+    int e = apply(q);  // q = A p, sigma = <p, q> (krylov.hpp:248-249)
     if (e) return e;
     if ((e = reduce(Dot{}, POST_SIGMA, p, q, nullptr, nullptr, 1))) return e;
     if ((e = reduce(Upd{}, POST_RHO, p, q, x, r, 1))) return e;

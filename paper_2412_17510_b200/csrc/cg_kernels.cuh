@@ -115,48 +115,15 @@ MPSG_DI void cg_post(CgState<K>* st, int post, const MC<K>& d) {
   }
 }
 
-// Generic reduction kernel body.  MODE selects the per-element work:
-//   0: d += u_i * v_i                                   (dots)
-//   1: x_i += alpha p_i; r_i += (-alpha) q_i; d += r_i r_i (axpy pair + dot)
-//   2: w_i = b_i - w_i; d += w_i w_i                    (true residual)
-// local_out != nullptr (multi-GPU): the last block stores this rank's total
-// there instead of running the scalar step; cg_post_gathered_kernel finishes
-// after the partials of all ranks are allgathered.
-template <int K, int MODE>
-__global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, int post, int64_t n,
-                                                                const double* u, const double* v,
-                                                                double* x, double* r, double* partial,
-                                                                int gate, double* local_out) {
-  __shared__ MC<K> sh[DOT_THREADS / 32];
+// Block partial -> global partial[blockIdx]; the last block to arrive sums
+// the G partials in a fixed order (thread t a contiguous run, then the block
+// tree) and runs the scalar step (or, multi-GPU, stores this rank's total in
+// local_out for the rank-ordered allgather sum).  Deterministic for a fixed
+// grid size.
+template <int K, int NT>
+MPSG_DI void reduce_finish(CgState<K>* st, int post, MC<K> acc, double* partial, double* local_out, MC<K>* sh) {
   __shared__ bool last;
-  if (gate && st->status != CG_RUNNING) return;
   const int G = gridDim.x;
-  const int64_t seg = (n + G - 1) / G;
-  const int64_t lo = (int64_t)blockIdx.x * seg;
-  const int64_t hi = (lo + seg < n) ? lo + seg : n;
-  MC<K> acc = zero<K>();
-  if constexpr (MODE == 0) {
-    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS)
-      acc = add(acc, mul(load_aos_rw<K>(u, i), load_aos_rw<K>(v, i)));
-  } else if constexpr (MODE == 1) {
-    // u = p, v = q; x, r updated in place (krylov.hpp:256-257: axpy = y + alpha*x)
-    const MC<K> alpha = st->alpha;
-    const MC<K> malpha = negate(alpha);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) {
-      MC<K> xi = add(load_aos_rw<K>(x, i), mul(alpha, load_aos_rw<K>(u, i)));
-      MC<K> ri = add(load_aos_rw<K>(r, i), mul(malpha, load_aos_rw<K>(v, i)));
-      store_aos<K>(x, i, xi);
-      store_aos<K>(r, i, ri);
-      acc = add(acc, mul(ri, ri));
-    }
-  } else {
-    // u = b, x = A x (overwritten with b - A x)
-    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) {
-      MC<K> w = sub(load_aos_rw<K>(u, i), load_aos_rw<K>(x, i));
-      store_aos<K>(x, i, w);
-      acc = add(acc, mul(w, w));
-    }
-  }
   MC<K> bsum = block_reduce(acc, sh);
   if (threadIdx.x == 0) {
     double* pp = partial + (int64_t)blockIdx.x * K;
@@ -168,9 +135,7 @@ __global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // last block: fixed-order sum of the G partials (thread t takes a
-  // contiguous run, then the block tree), then the scalar step.
-  const int per = (G + DOT_THREADS - 1) / DOT_THREADS;
+  const int per = (G + NT - 1) / NT;
   MC<K> s = zero<K>();
   for (int i = threadIdx.x * per; i < (threadIdx.x + 1) * per && i < G; ++i) {
     MC<K> pv;
@@ -189,6 +154,48 @@ __global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, 
       cg_post(st, post, tot);
     }
   }
+}
+
+// Generic reduction kernel.  MODE selects the per-element work:
+//   0: d += u_i * v_i                                   (dots)
+//   1: x_i += alpha p_i; r_i += (-alpha) q_i; d += r_i r_i (axpy pair + dot)
+//   2: w_i = b_i - w_i; d += w_i w_i                    (true residual)
+// The grid is sized to one resident wave (SMs x occupancy); each block owns a
+// contiguous segment that its threads stride through (coalesced).
+// local_out != nullptr (multi-GPU): see reduce_finish.
+template <int K, int MODE>
+__global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, int post, int64_t n,
+                                                                const double* u, const double* v,
+                                                                double* x, double* r, double* partial,
+                                                                int gate, double* local_out) {
+  __shared__ MC<K> sh[DOT_THREADS / 32];
+  if (gate && st->status != CG_RUNNING) return;
+  const int G = gridDim.x;
+  const int64_t seg = (n + G - 1) / G;
+  const int64_t lo = (int64_t)blockIdx.x * seg;
+  const int64_t hi = (lo + seg < n) ? lo + seg : n;
+  MC<K> acc = zero<K>();
+  const MC<K> alpha = MODE == 1 ? st->alpha : zero<K>();
+  const MC<K> malpha = negate(alpha);
+  auto term = [&](int64_t i) -> MC<K> {
+    if constexpr (MODE == 0) {
+      return mul(load_aos_rw<K>(u, i), load_aos_rw<K>(v, i));
+    } else if constexpr (MODE == 1) {
+      // u = p, v = q; x, r updated in place (krylov.hpp:256-257: axpy = y + alpha*x)
+      MC<K> xi = add(load_aos_rw<K>(x, i), mul(alpha, load_aos_rw<K>(u, i)));
+      MC<K> ri = add(load_aos_rw<K>(r, i), mul(malpha, load_aos_rw<K>(v, i)));
+      store_aos<K>(x, i, xi);
+      store_aos<K>(r, i, ri);
+      return mul(ri, ri);
+    } else {
+      // u = b, x = A x (overwritten with b - A x)
+      MC<K> w = sub(load_aos_rw<K>(u, i), load_aos_rw<K>(x, i));
+      store_aos<K>(x, i, w);
+      return mul(w, w);
+    }
+  };
+  for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) acc = add(acc, term(i));
+  reduce_finish<K, DOT_THREADS>(st, post, acc, partial, local_out, sh);
 }
 
 // Rank-ordered multi-component sum of the allgathered partials, then the

@@ -209,13 +209,12 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
 // ---------------------------------------------------------------------------
 // SELL slice, real: one warp per slice of 32 rows, one thread per row.
 // ---------------------------------------------------------------------------
+// Row sum of slot `lane` of SELL slice s in the chosen order; row = the
+// original row (-1 for padding).
 template <int K, int ORDER>
-MPSG_DI void sell_real_body(const SellView& S, const double* __restrict__ x, double* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (s >= S.nslices) return;
+MPSG_DI MC<K> sell_row(const SellView& S, const double* __restrict__ x, int s, int lane, int& row) {
   const int slot = s * 32 + lane;
-  const int row = S.slot_row[slot];
+  row = S.slot_row[slot];
   const int len = S.slot_len[slot];
   const int64_t base = S.slice_ptr[s] + lane;
   const int* __restrict__ cp = S.col + base;
@@ -230,6 +229,15 @@ MPSG_DI void sell_real_body(const SellView& S, const double* __restrict__ x, dou
   } else {
     acc = lane4_row<K, MPSG_SELL_PAR(K)>(vp, cp, st, x, len);
   }
+  return acc;
+}
+
+template <int K, int ORDER>
+MPSG_DI void sell_real_body(const SellView& S, const double* __restrict__ x, double* __restrict__ y) {
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= S.nslices) return;
+  int row;
+  const MC<K> acc = sell_row<K, ORDER>(S, x, s, threadIdx.x & 31, row);
   if (row >= 0) store_aos<K>(y, row, acc);
 }
 
