@@ -85,6 +85,14 @@ enum mpsg_solver_status {
   MPSG_DIVERGED = 3
 };
 
+/* mpsg_csr_upload_ex flags */
+enum mpsg_csr_flags {
+  MPSG_CSR_COMPLEX = 1,   /* 2x the planes: re then im over one structure (ComplexSparseMatrix) */
+  MPSG_CSR_MIXED = 2,     /* binary64 values: 1 plane (2 complex), vectors in K components
+                             (CsrMatrix<double> x MultiComponent<K>, the paper's "M" mode) */
+  MPSG_CSR_TRANSPOSE = 4  /* also build the device transpose for mpsg_sptmv* */
+};
+
 typedef struct mpsg_ctx mpsg_ctx;
 typedef struct mpsg_csr mpsg_csr;
 
@@ -97,7 +105,9 @@ typedef struct mpsg_csr_stats {
   int64_t nlong;           /* rows in the long-row store */
   int64_t long_nnz;        /* nonzeros in the long-row store */
   int64_t nchunks;         /* fast-mode warp chunks over long rows */
-  int64_t device_bytes;    /* device memory held by the matrix */
+  int64_t device_bytes;    /* device memory held by the matrix (and its transpose) */
+  int32_t is_mixed;        /* binary64 values */
+  int32_t has_transpose;   /* uploaded with MPSG_CSR_TRANSPOSE */
 } mpsg_csr_stats;
 
 /* SolverConfig subset used by CG (krylov.hpp:58-75). */
@@ -143,6 +153,11 @@ MPSG_API int mpsg_ctx_synchronize(mpsg_ctx* ctx);
 MPSG_API int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t ncols,
                     const int64_t* indptr, const int64_t* indices, const double* const* planes,
                     mpsg_csr** out);
+/* General form: flags from mpsg_csr_flags; planes has K (Pure) or 1 (Mixed)
+ * entries per part, times 2 for complex. */
+MPSG_API int mpsg_csr_upload_ex(mpsg_ctx* ctx, int K, int flags, int64_t nrows, int64_t ncols,
+                                const int64_t* indptr, const int64_t* indices, const double* const* planes,
+                                mpsg_csr** out);
 MPSG_API void mpsg_csr_destroy(mpsg_csr* A);
 MPSG_API int mpsg_csr_get_stats(const mpsg_csr* A, mpsg_csr_stats* out);
 
@@ -157,6 +172,21 @@ MPSG_API int mpsg_spmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int6
                       const double* x_re, const double* x_im, double* y_re, double* y_im);
 MPSG_API int mpsg_spmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_x_re,
                           const double* d_x_im, double* d_y_re, double* d_y_im, void* stream);
+
+/* ---- transposed products (kernels.hpp:368-394, 419-441) ---------------- */
+/* y[ncols*K] = A^T v[nrows*K]; needs MPSG_CSR_TRANSPOSE at upload.  The
+ * exact orders reproduce the reference sptmv at one thread (bit for bit, lanes
+ * on or off -- the lane batches there are per-element exact); FAST reorders
+ * long columns. */
+MPSG_API int mpsg_sptmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t vlen, const double* v, double* y);
+MPSG_API int mpsg_sptmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_v, double* d_y,
+                            void* stream);
+/* conjugate != 0: the adjoint A^H v (y.re = rr + ii, y.im = ri - ir). */
+MPSG_API int mpsg_sptmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugate, int64_t vlen,
+                                const double* v_re, const double* v_im, double* y_re, double* y_im);
+MPSG_API int mpsg_sptmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugate,
+                                    const double* d_v_re, const double* d_v_im, double* d_y_re, double* d_y_im,
+                                    void* stream);
 
 /* ---- conjugate gradient (krylov.hpp:238-281) -------------------------- */
 /* Device-resident CG on A (real, square).  b and x0 (NULL = zero start) are

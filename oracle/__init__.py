@@ -54,8 +54,13 @@ def orc():
         L.orc_to_double.restype = _f64
         L.orc_spmv.argtypes = [_i32, _i32, _i32, _i64, _i64, _i64, _P, _P, _P, _P, _P]
         L.orc_spmv.restype = _i32
-        L.orc_spmv_complex.argtypes = [_i32, _i32, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.orc_spmv_complex.argtypes = [_i32, _i32, _i32, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P, _P]
         L.orc_spmv_complex.restype = _i32
+        L.orc_sptmv.argtypes = [_i32, _i32, _i32, _i64, _i64, _i64, _P, _P, _P, _P, _P]
+        L.orc_sptmv.restype = _i32
+        L.orc_sptmv_complex.argtypes = [_i32, _i32, _i32, _i32, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P,
+                                        _P]
+        L.orc_sptmv_complex.restype = _i32
         L.orc_checksum.argtypes = [_i32, _i64, _P]
         L.orc_checksum.restype = _u64
         L.orc_checksum_complex.argtypes = [_i32, _i64, _P, _P]
@@ -97,15 +102,47 @@ def spmv(A, x, order=LANE4, mixed=False):
     return y
 
 
-def spmv_complex(A, xre, xim, order=LANE4):
+def _cplanes(A, K, mixed):
+    """(re, im) value planes of a complex matrix: [K, nnz] each, or one
+    binary64 plane each in mixed mode (planes [2, nnz])."""
+    P = np.asarray(A.planes)
+    return (_c(P[0]), _c(P[1])) if mixed else (_c(P[:K]), _c(P[K:2 * K]))
+
+
+def spmv_complex(A, xre, xim, order=LANE4, mixed=False):
     K = xre.shape[1]
     yre = np.empty((A.nrows, K))
     yim = np.empty((A.nrows, K))
-    rc = orc().orc_spmv_complex(K, order, A.nrows, A.ncols, xre.shape[0], _p(_c(A.indptr, np.int64)),
-                                _p(_c(A.indices, np.int64)), _p(_c(A.planes[:K])), _p(_c(A.planes[K:])),
+    vre, vim = _cplanes(A, K, mixed)
+    rc = orc().orc_spmv_complex(K, order, 1 if mixed else 0, A.nrows, A.ncols, xre.shape[0],
+                                _p(_c(A.indptr, np.int64)), _p(_c(A.indices, np.int64)), _p(vre), _p(vim),
                                 _p(_c(xre)), _p(_c(xim)), _p(yre), _p(yim))
     if rc != 0:
         raise ValueError("spmv_complex: dimension mismatch")
+    return yre, yim
+
+
+def sptmv(A, v, threads=1, mixed=False):
+    """y = A^T v in the reference's order (kernels.hpp:368-394) for `threads` OpenMP threads."""
+    K = v.shape[1]
+    y = np.empty((A.ncols, K))
+    vals = _c(A.planes[0] if mixed else A.planes[:K])
+    rc = orc().orc_sptmv(K, 1 if mixed else 0, threads, A.nrows, A.ncols, v.shape[0], _p(_c(A.indptr, np.int64)),
+                         _p(_c(A.indices, np.int64)), _p(vals), _p(_c(v)), _p(y))
+    if rc != 0:
+        raise ValueError(f"sptmv: vector length {v.shape[0]} does not match matrix dimension {A.nrows}")
+    return y
+
+
+def sptmv_complex(A, vre, vim, threads=1, conjugate=False, mixed=False):
+    K = vre.shape[1]
+    yre, yim = np.empty((A.ncols, K)), np.empty((A.ncols, K))
+    pre, pim = _cplanes(A, K, mixed)
+    rc = orc().orc_sptmv_complex(K, 1 if mixed else 0, threads, 1 if conjugate else 0, A.nrows, A.ncols,
+                                 vre.shape[0], _p(_c(A.indptr, np.int64)), _p(_c(A.indices, np.int64)), _p(pre),
+                                 _p(pim), _p(_c(vre)), _p(_c(vim)), _p(yre), _p(yim))
+    if rc != 0:
+        raise ValueError("sptmv_complex: dimension mismatch")
     return yre, yim
 
 
@@ -196,6 +233,8 @@ def ref():
         L.ref_cvec_checksum.restype = _u64
         L.ref_spmv_complex.argtypes = [_P, _P, _i32, _i32, _P]
         L.ref_spmv_complex.restype = _i32
+        L.ref_sptmv_complex.argtypes = [_P, _P, _i32, _i32, _i32, _P]
+        L.ref_sptmv_complex.restype = _i32
         L.ref_mc_op.argtypes = [_i32, _i32, _P, _P, _P]
         L.ref_make_vector.argtypes = [_i32, _i64, _P]
         L.ref_make_complex_vector.argtypes = [_i32, _i64, _P, _P]
@@ -263,11 +302,14 @@ def ref_spmv(A, x, order=LANE4, threads=1, mixed=False):
 
 
 class RefComplex:
-    def __init__(self, A, K):
+    """Reference ``ComplexSparseMatrix<E>``; mixed: E = double (planes [2, nnz])."""
+
+    def __init__(self, A, K, mixed=False):
         self.K = K
-        self.h = ref().ref_ccsr_create(K, A.nrows, A.ncols, _p(_c(A.indptr, np.int64)),
-                                       _p(_c(A.indices, np.int64)), _p(_c(A.planes[:K])),
-                                       _p(_c(A.planes[K:])))
+        P = np.asarray(A.planes)
+        re_, im_ = (P[0], P[1]) if mixed else (P[:K], P[K:2 * K])
+        self.h = ref().ref_ccsr_create(1 if mixed else K, A.nrows, A.ncols, _p(_c(A.indptr, np.int64)),
+                                       _p(_c(A.indices, np.int64)), _p(_c(re_)), _p(_c(im_)))
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -330,6 +372,30 @@ def ref_make_complex_vector(K, n):
     re, im = np.empty((n, K)), np.empty((n, K))
     ref().ref_make_complex_vector(K, n, _p(re), _p(im))
     return re, im
+
+
+def ref_spmv_complex(A, xr, xi, order=LANE4, threads=1, mixed=False):
+    K = xr.shape[1]
+    Ah, xh, yh = RefComplex(A, K, mixed), RefCVec(xr, xi), RefCVec(K=K)
+    if ref().ref_spmv_complex(Ah.h, xh.h, order, threads, yh.h) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return yh.read(A.nrows)
+
+
+def ref_sptmv(A, v, order=LANE4, threads=1, mixed=False):
+    K = v.shape[1]
+    Ah, xh, yh = RefCsr(A, K, mixed), RefVec(v), RefVec(K=K)
+    if ref().ref_sptmv(Ah.h, xh.h, order, threads, yh.h) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return yh.read()
+
+
+def ref_sptmv_complex(A, vr, vi, order=LANE4, threads=1, conjugate=False, mixed=False):
+    K = vr.shape[1]
+    Ah, xh, yh = RefComplex(A, K, mixed), RefCVec(vr, vi), RefCVec(K=K)
+    if ref().ref_sptmv_complex(Ah.h, xh.h, order, threads, 1 if conjugate else 0, yh.h) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return yh.read(A.ncols)
 
 
 def ref_cg(A, b, order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters=10000):

@@ -377,7 +377,7 @@ ORC_API int orc_spmv(int K, int lanes, int mixed, int64_t nrows, int64_t ncols, 
 /* kernels.hpp:399-416: four real products then y.re = rr - ii (sub =
  * add(x, negate(y)), multicomp.hpp:286-289), y.im = ri + ir. re and im share
  * one structure here (check_split_structure, sparse.hpp:254-259). */
-ORC_API int orc_spmv_complex(int K, int lanes, int64_t nrows, int64_t ncols, int64_t xlen,
+ORC_API int orc_spmv_complex(int K, int lanes, int mixed, int64_t nrows, int64_t ncols, int64_t xlen,
                              const int64_t *indptr, const int64_t *indices, const double *vre,
                              const double *vim, const double *xre, const double *xim, double *yre,
                              double *yim) {
@@ -385,13 +385,99 @@ ORC_API int orc_spmv_complex(int K, int lanes, int64_t nrows, int64_t ncols, int
   int64_t nnz = indptr[nrows];
   for (int64_t i = 0; i < nrows; ++i) {
     double rr[4], ii[4], ri[4], ir[4];
-    row_sum(K, lanes, 0, indptr[i], indptr[i + 1], indices, vre, nnz, xre, rr);
-    row_sum(K, lanes, 0, indptr[i], indptr[i + 1], indices, vim, nnz, xim, ii);
-    row_sum(K, lanes, 0, indptr[i], indptr[i + 1], indices, vre, nnz, xim, ri);
-    row_sum(K, lanes, 0, indptr[i], indptr[i + 1], indices, vim, nnz, xre, ir);
+    row_sum(K, lanes, mixed, indptr[i], indptr[i + 1], indices, vre, nnz, xre, rr);
+    row_sum(K, lanes, mixed, indptr[i], indptr[i + 1], indices, vim, nnz, xim, ii);
+    row_sum(K, lanes, mixed, indptr[i], indptr[i + 1], indices, vre, nnz, xim, ri);
+    row_sum(K, lanes, mixed, indptr[i], indptr[i + 1], indices, vim, nnz, xre, ir);
     orc_sub(K, rr, ii, yre + i * K);
     orc_add(K, ri, ir, yim + i * K);
   }
+  return 0;
+}
+
+/* ------------------------------------------------------------- SpTMV ---
+ * kernels.hpp:368-394 (sptmv): with one thread, one accumulator y (all +0)
+ * updated row by row, y[col_k] = y[col_k] + mul_term(a_k, v_i), i ascending
+ * (sptmv_block :214-225; the lane variant SptRow :227-322 performs the same
+ * per-element ops, so lanes do not change the bits).  With T > 1 threads:
+ * partition_rows(T) blocks (:63-80), one zero accumulator per block, merged
+ * in thread order y = acc_0; y[j] = y[j] + acc_t[j] (:386-392). */
+static void sptmv_block(int K, int mixed, int64_t r0, int64_t r1, const int64_t *indptr,
+                        const int64_t *indices, const double *vals, int64_t nnz, const double *v,
+                        double *acc) {
+  double a[4], p[4];
+  for (int64_t i = r0; i < r1; ++i) {
+    const double *vi = v + i * K;
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) {
+      double *yj = acc + indices[k] * K;
+      if (mixed) {
+        orc_mul_d(K, vi, vals[k], p);
+      } else {
+        for (int j = 0; j < K; ++j) a[j] = vals[(int64_t)j * nnz + k];
+        orc_mul(K, a, vi, p);
+      }
+      orc_add(K, yj, p, yj);
+    }
+  }
+}
+static int64_t lower_bound_i64(const int64_t *a, int64_t n, int64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+ORC_API int orc_sptmv(int K, int mixed, int threads, int64_t nrows, int64_t ncols, int64_t vlen,
+                      const int64_t *indptr, const int64_t *indices, const double *vals,
+                      const double *v, double *y) {
+  if (vlen != nrows) return -1;
+  int64_t nnz = indptr[nrows];
+  if (threads < 1) threads = 1;
+  memset(y, 0, sizeof(double) * (size_t)(ncols * K));
+  if (threads == 1 || nrows == 0) {
+    sptmv_block(K, mixed, 0, nrows, indptr, indices, vals, nnz, v, y);
+    return 0;
+  }
+  double *acc = (double *)malloc(sizeof(double) * (size_t)(ncols * K) + 8);
+  int64_t b0 = 0;
+  for (int t = 0; t < threads; ++t) {
+    /* partition_rows: bounds[t] = lower_bound(indptr, total*t/parts) */
+    int64_t b1 = (t + 1 == threads) ? nrows : lower_bound_i64(indptr, nrows, nnz * (t + 1) / threads);
+    if (b1 < b0) b1 = b0;
+    double *dst = (t == 0) ? y : acc;
+    if (t > 0) memset(acc, 0, sizeof(double) * (size_t)(ncols * K));
+    sptmv_block(K, mixed, b0, b1, indptr, indices, vals, nnz, v, dst);
+    if (t > 0)
+      for (int64_t j = 0; j < ncols; ++j) orc_add(K, y + j * K, acc + j * K, y + j * K);
+    b0 = b1;
+  }
+  free(acc);
+  return 0;
+}
+/* kernels.hpp:419-441: four real transposed products, then rr - ii / ri + ir,
+ * or with conjugate (the adjoint) rr + ii / ri - ir. */
+ORC_API int orc_sptmv_complex(int K, int mixed, int threads, int conj, int64_t nrows, int64_t ncols,
+                              int64_t vlen, const int64_t *indptr, const int64_t *indices,
+                              const double *vre, const double *vim, const double *xre, const double *xim,
+                              double *yre, double *yim) {
+  if (vlen != nrows) return -1;
+  size_t nb = sizeof(double) * (size_t)(ncols * K) + 8;
+  double *rr = malloc(nb), *ii = malloc(nb), *ri = malloc(nb), *ir = malloc(nb);
+  orc_sptmv(K, mixed, threads, nrows, ncols, vlen, indptr, indices, vre, xre, rr);
+  orc_sptmv(K, mixed, threads, nrows, ncols, vlen, indptr, indices, vim, xim, ii);
+  orc_sptmv(K, mixed, threads, nrows, ncols, vlen, indptr, indices, vre, xim, ri);
+  orc_sptmv(K, mixed, threads, nrows, ncols, vlen, indptr, indices, vim, xre, ir);
+  for (int64_t j = 0; j < ncols; ++j) {
+    if (conj) {
+      orc_add(K, rr + j * K, ii + j * K, yre + j * K);
+      orc_sub(K, ri + j * K, ir + j * K, yim + j * K);
+    } else {
+      orc_sub(K, rr + j * K, ii + j * K, yre + j * K);
+      orc_add(K, ri + j * K, ir + j * K, yim + j * K);
+    }
+  }
+  free(rr); free(ii); free(ri); free(ir);
   return 0;
 }
 

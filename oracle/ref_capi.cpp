@@ -40,8 +40,10 @@ struct CsrH {
   AnyCsr m;
 };
 struct ComplexH {
-  int K;
-  std::variant<ComplexSparseMatrix<MC<2>>, ComplexSparseMatrix<MC<3>>, ComplexSparseMatrix<MC<4>>> m;
+  int K;  // 1 = binary64 matrix (mixed mode)
+  std::variant<ComplexSparseMatrix<MC<2>>, ComplexSparseMatrix<MC<3>>, ComplexSparseMatrix<MC<4>>,
+               ComplexSparseMatrix<double>>
+      m;
 };
 struct VecH {
   int K;
@@ -204,6 +206,10 @@ void* ref_ccsr_create(int K, int64_t nrows, int64_t ncols, const int64_t* indptr
                       const int64_t* indices, const double* re_vals, const double* im_vals) {
   auto* h = new ComplexH{K, ComplexSparseMatrix<MC<2>>{}};
   switch (K) {
+    case 1:
+      h->m = ComplexSparseMatrix<double>{build_csr<double>(nrows, ncols, indptr, indices, re_vals),
+                                         build_csr<double>(nrows, ncols, indptr, indices, im_vals)};
+      break;
     case 2:
       h->m = ComplexSparseMatrix<MC<2>>{build_csr<MC<2>>(nrows, ncols, indptr, indices, re_vals),
                                         build_csr<MC<2>>(nrows, ncols, indptr, indices, im_vals)};
@@ -249,16 +255,35 @@ int ref_spmv_complex(void* A, void* v, int lanes, int threads, void* out) {
   return guard([&] {
     std::visit(
         [&](auto& mat, auto& vec) {
-          using MatT = std::decay_t<decltype(mat)>;
-          using VecT = std::decay_t<decltype(vec)>;
-          if constexpr (std::is_same_v<decltype(mat.re.values.get(0)),
-                                       typename decltype(vec.re)::value_type>) {
-            (void)sizeof(MatT);
-            (void)sizeof(VecT);
+          using E = std::decay_t<decltype(mat.re.values.get(0))>;
+          using F = typename decltype(vec.re)::value_type;
+          if constexpr (std::is_same_v<E, F> || std::is_same_v<E, double>) {
             y->v = spmv_complex(mat, vec, mode);
             y->K = x->K;
           } else {
             throw std::runtime_error("ref_spmv_complex: precision mismatch");
+          }
+        },
+        a->m, x->v);
+  });
+}
+
+// mps::sptmv_complex (kernels.hpp:419-441), conjugate = adjoint
+int ref_sptmv_complex(void* A, void* v, int lanes, int threads, int conjugate, void* out) {
+  auto* a = static_cast<ComplexH*>(A);
+  auto* x = static_cast<CVecH*>(v);
+  auto* y = static_cast<CVecH*>(out);
+  KernelMode mode = mode_of(lanes, threads);
+  return guard([&] {
+    std::visit(
+        [&](auto& mat, auto& vec) {
+          using E = std::decay_t<decltype(mat.re.values.get(0))>;
+          using F = typename decltype(vec.re)::value_type;
+          if constexpr (std::is_same_v<E, F> || std::is_same_v<E, double>) {
+            y->v = sptmv_complex(mat, vec, mode, conjugate != 0);
+            y->K = x->K;
+          } else {
+            throw std::runtime_error("ref_sptmv_complex: precision mismatch");
           }
         },
         a->m, x->v);

@@ -54,7 +54,8 @@ class MpsgError(RuntimeError):
 class CsrStats(ctypes.Structure):
     _fields_ = [("nrows", _i64), ("ncols", _i64), ("nnz", _i64), ("K", ctypes.c_int32),
                 ("is_complex", ctypes.c_int32), ("nslices", _i64), ("sell_elems", _i64),
-                ("nlong", _i64), ("long_nnz", _i64), ("nchunks", _i64), ("device_bytes", _i64)]
+                ("nlong", _i64), ("long_nnz", _i64), ("nchunks", _i64), ("device_bytes", _i64),
+                ("is_mixed", ctypes.c_int32), ("has_transpose", ctypes.c_int32)]
 
 
 class _CgConfig(ctypes.Structure):
@@ -79,7 +80,10 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_checksum_complex", "mpsg_version", "mpsg_measure_fp64_peak", "mpsg_mc_op_dev",
            "mpsg_comm_unique_id", "mpsg_comm_create", "mpsg_comm_destroy", "mpsg_dcsr_upload",
            "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
-           "mpsg_dcg", "mpsg_halo_plan")
+           "mpsg_dcg", "mpsg_halo_plan", "mpsg_csr_upload_ex", "mpsg_sptmv", "mpsg_sptmv_dev",
+           "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev")
+
+CSR_COMPLEX, CSR_MIXED, CSR_TRANSPOSE = 1, 2, 4
 
 
 def lib():
@@ -129,6 +133,11 @@ def lib():
     L.mpsg_dcg.argtypes = [_P, _i32, _P, _P, ctypes.POINTER(_CgConfig), _P, _P, _i64,
                            ctypes.POINTER(_CgReport)]
     L.mpsg_halo_plan.argtypes = [_i32, _i32, _P, _P, _P, _P]
+    L.mpsg_csr_upload_ex.argtypes = [_P, _i32, _i32, _i64, _i64, _P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P)]
+    L.mpsg_sptmv.argtypes = [_P, _P, _i32, _i64, _P, _P]
+    L.mpsg_sptmv_dev.argtypes = [_P, _P, _i32, _P, _P, _P]
+    L.mpsg_sptmv_complex.argtypes = [_P, _P, _i32, _i32, _i64, _P, _P, _P, _P]
+    L.mpsg_sptmv_complex_dev.argtypes = [_P, _P, _i32, _i32, _P, _P, _P, _P, _P]
     _lib = L
     return L
 
@@ -201,25 +210,30 @@ class DeviceCsr:
     ``ComplexSparseMatrix`` sharing one structure).
 
     ``A`` is any object with ``nrows, ncols, indptr (int64), indices (int64),
-    planes`` ([K, nnz] real, [2K, nnz] complex).
+    planes``: [K, nnz] real, [2K, nnz] complex (re planes then im planes);
+    with ``mixed`` (the binary64 matrix of Mixed mode, ``CsrMatrix<double>``)
+    one plane real, two complex.  ``transpose`` also uploads A^T for sptmv.
     """
 
-    def __init__(self, A, K: int, is_complex: bool = False, ctx: Optional[Context] = None):
+    def __init__(self, A, K: int, is_complex: bool = False, ctx: Optional[Context] = None,
+                 mixed: bool = False, transpose: bool = False):
         self.ctx = ctx or default_context()
         self.K = K
         self.is_complex = bool(is_complex)
+        self.mixed = bool(mixed)
         self.nrows, self.ncols = int(A.nrows), int(A.ncols)
         indptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
         indices = np.ascontiguousarray(A.indices, dtype=np.int64)
-        nplanes = 2 * K if is_complex else K
+        nplanes = (1 if mixed else K) * (2 if is_complex else 1)
         planes = np.asarray(A.planes)
         if planes.shape[0] < nplanes:
             raise ValueError(f"DeviceCsr: need {nplanes} value planes, got {planes.shape[0]}")
         plist = [np.ascontiguousarray(planes[j], dtype=np.float64) for j in range(nplanes)]
         parr = (_P * nplanes)(*[p.ctypes.data for p in plist])
+        flags = (CSR_COMPLEX if is_complex else 0) | (CSR_MIXED if mixed else 0) | (CSR_TRANSPOSE if transpose else 0)
         h = _P()
-        self.ctx.check(lib().mpsg_csr_upload(self.ctx.h, K, 1 if is_complex else 0, self.nrows, self.ncols,
-                                             _p(indptr), _p(indices), parr, ctypes.byref(h)))
+        self.ctx.check(lib().mpsg_csr_upload_ex(self.ctx.h, K, flags, self.nrows, self.ncols, _p(indptr),
+                                                _p(indices), parr, ctypes.byref(h)))
         self.h = h
         self.nnz = int(indptr[-1])
 
@@ -283,6 +297,38 @@ def spmv_complex(A: DeviceCsr, v_re, v_im, mode: KernelMode | int | None = None)
     A.ctx.check(lib().mpsg_spmv_complex(A.ctx.h, A.h, _order(mode), xr.shape[0], _p(xr), _p(xi), _p(yr),
                                         _p(yi)))
     return yr, yi
+
+
+def sptmv(A: DeviceCsr, v, mode: KernelMode | int | None = None) -> np.ndarray:
+    """y = A^T v (kernels.hpp:368-394); the exact orders equal the reference
+    sptmv at one thread.  Needs ``DeviceCsr(..., transpose=True)``."""
+    x = _aos(v, "sptmv")
+    if x.shape[1] != A.K:
+        raise ValueError(f"sptmv: vector has K={x.shape[1]} components, matrix has K={A.K}")
+    y = np.empty((A.ncols, A.K))
+    A.ctx.check(lib().mpsg_sptmv(A.ctx.h, A.h, _order(mode), x.shape[0], _p(x), _p(y)))
+    return y
+
+
+def sptmv_complex(A: DeviceCsr, v_re, v_im, mode: KernelMode | int | None = None, conjugate: bool = False):
+    """(y_re, y_im) = A^T v, or the adjoint A^H v with ``conjugate`` (kernels.hpp:419-441)."""
+    xr, xi = _aos(v_re, "sptmv_complex"), _aos(v_im, "sptmv_complex")
+    if xr.shape[0] != xi.shape[0]:
+        raise ValueError("sptmv_complex: re/im vector length mismatch")
+    yr, yi = np.empty((A.ncols, A.K)), np.empty((A.ncols, A.K))
+    A.ctx.check(lib().mpsg_sptmv_complex(A.ctx.h, A.h, _order(mode), 1 if conjugate else 0, xr.shape[0], _p(xr),
+                                         _p(xi), _p(yr), _p(yi)))
+    return yr, yi
+
+
+def sptmv_dev(A: DeviceCsr, d_v: int, d_y: int, order: int = ORDER_LANE4, stream: int | None = None):
+    A.ctx.check(lib().mpsg_sptmv_dev(A.ctx.h, A.h, order, d_v, d_y, stream))
+
+
+def sptmv_complex_dev(A: DeviceCsr, d_vr: int, d_vi: int, d_yr: int, d_yi: int, order: int = ORDER_LANE4,
+                      conjugate: bool = False, stream: int | None = None):
+    A.ctx.check(lib().mpsg_sptmv_complex_dev(A.ctx.h, A.h, order, 1 if conjugate else 0, d_vr, d_vi, d_yr, d_yi,
+                                             stream))
 
 
 def spmv_dev(A: DeviceCsr, d_x: int, d_y: int, order: int = ORDER_LANE4, stream: int | None = None):
@@ -365,6 +411,9 @@ class CsrOperator:
 
     def apply(self, x):
         return spmv(self.matrix, x, self.mode())
+
+    def apply_transposed(self, x):
+        return sptmv(self.matrix, x, self.mode())
 
 
 def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:

@@ -88,6 +88,7 @@ __global__ void build_long_kernel(const int* lrow, const int64_t* lptr, const in
 
 void free_csr(mpsg_csr* A) {
   if (!A) return;
+  free_csr(A->trans);
   void* ptrs[] = {A->slice_ptr, A->slot_row,    A->slot_len, A->scol,      A->sval,
                   A->lrow,      A->lptr,        A->lcol,     A->lval,      A->chunk_row,
                   A->chunk_beg, A->chunk_end,   A->chunk_slot, A->chunk_first, A->partial,
@@ -108,20 +109,20 @@ std::string dim_msg(const char* what, int64_t vsize, int64_t ncols) {
 
 namespace mpsg {
 int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
-                double* yre, double* yim, cudaStream_t st) {
+                double* yre, double* yim, cudaStream_t st, bool conj) {
   if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "spmv: unknown order %d", order);
   if (A->nrows == 0) return MPSG_OK;
   if (!A->cplx) {
     switch (A->K) {
-      case 2: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st);
-      case 3: return launch_spmv_k<3, false>(ctx, A, order, xre, xim, yre, yim, st);
-      case 4: return launch_spmv_k<4, false>(ctx, A, order, xre, xim, yre, yim, st);
+      case 2: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st, conj);
+      case 3: return launch_spmv_k<3, false>(ctx, A, order, xre, xim, yre, yim, st, conj);
+      case 4: return launch_spmv_k<4, false>(ctx, A, order, xre, xim, yre, yim, st, conj);
     }
   } else {
     switch (A->K) {
-      case 2: return launch_spmv_k<2, true>(ctx, A, order, xre, xim, yre, yim, st);
-      case 3: return launch_spmv_k<3, true>(ctx, A, order, xre, xim, yre, yim, st);
-      case 4: return launch_spmv_k<4, true>(ctx, A, order, xre, xim, yre, yim, st);
+      case 2: return launch_spmv_k<2, true>(ctx, A, order, xre, xim, yre, yim, st, conj);
+      case 3: return launch_spmv_k<3, true>(ctx, A, order, xre, xim, yre, yim, st, conj);
+      case 4: return launch_spmv_k<4, true>(ctx, A, order, xre, xim, yre, yim, st, conj);
     }
   }
   return fail(ctx, MPSG_E_ARG, "spmv: unsupported K %d", A->K);
@@ -210,9 +211,18 @@ int mpsg_ctx_synchronize(mpsg_ctx* ctx) {
 int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t ncols,
                     const int64_t* indptr, const int64_t* indices, const double* const* planes,
                     mpsg_csr** out) {
+  return mpsg_csr_upload_ex(ctx, K, is_complex ? MPSG_CSR_COMPLEX : 0, nrows, ncols, indptr, indices, planes, out);
+}
+
+int mpsg_csr_upload_ex(mpsg_ctx* ctx, int K, int flags, int64_t nrows, int64_t ncols, const int64_t* indptr,
+                       const int64_t* indices, const double* const* planes, mpsg_csr** out) {
   if (!ctx || !out) return MPSG_E_ARG;
   *out = nullptr;
+  const int is_complex = (flags & MPSG_CSR_COMPLEX) != 0;
+  const bool mixed = (flags & MPSG_CSR_MIXED) != 0;
   if (K < 2 || K > 4) return fail(ctx, MPSG_E_ARG, "csr_upload: K must be 2, 3 or 4 (got %d)", K);
+  if (flags & ~(MPSG_CSR_COMPLEX | MPSG_CSR_MIXED | MPSG_CSR_TRANSPOSE))
+    return fail(ctx, MPSG_E_ARG, "csr_upload: unknown flags 0x%x", flags);
   if (nrows < 0 || ncols < 0 || !indptr) return fail(ctx, MPSG_E_ARG, "csr_upload: bad shape");
   const int64_t I32 = std::numeric_limits<int>::max();
   if (nrows > I32 || ncols > I32)
@@ -220,7 +230,7 @@ int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t
                 (long long)nrows, (long long)ncols);
   if (indptr[0] != 0) return fail(ctx, MPSG_E_STRUCT, "csr_upload: indptr[0] must be 0");
   const int64_t nnz = indptr[nrows];
-  const int nplanes = is_complex ? 2 * K : K;
+  const int nplanes = (mixed ? 1 : K) * (is_complex ? 2 : 1);
   if (nnz > 0 && (!indices || !planes)) return fail(ctx, MPSG_E_ARG, "csr_upload: null arrays");
   for (int j = 0; j < nplanes && nnz > 0; ++j)
     if (!planes[j]) return fail(ctx, MPSG_E_ARG, "csr_upload: null plane %d", j);
@@ -231,6 +241,7 @@ int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t
   std::unique_ptr<mpsg_csr, void (*)(mpsg_csr*)> holder(A, free_csr);
   A->K = K;
   A->cplx = is_complex != 0;
+  A->mixed = mixed;
   A->nrows = nrows;
   A->ncols = ncols;
   A->nnz = nnz;
@@ -424,6 +435,29 @@ int mpsg_csr_upload(mpsg_ctx* ctx, int K, int is_complex, int64_t nrows, int64_t
   CUDA_TRY(ctx, cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (bad) return fail(ctx, MPSG_E_RANGE, "csr_upload: column index outside [0, %lld)", (long long)ncols);
+  if (flags & MPSG_CSR_TRANSPOSE) {
+    // A^T on the host (stable counting sort by column, as transpose_csr,
+    // sparse.hpp:139-163: the rows of A^T list their entries in ascending
+    // original row), uploaded as its own device matrix.  Row j of A^T summed
+    // in row order is exactly the reference sptmv's accumulation into y[j]
+    // at one thread (kernels.hpp:212-225): acc_j += A_ij v_i, i ascending.
+    std::vector<int64_t> tptr((size_t)ncols + 1, 0), tidx((size_t)nnz);
+    std::vector<double> tval((size_t)nnz * nplanes);
+    for (int64_t k = 0; k < nnz; ++k) tptr[(size_t)indices[k] + 1]++;
+    for (int64_t j = 0; j < ncols; ++j) tptr[(size_t)j + 1] += tptr[(size_t)j];
+    std::vector<int64_t> pos(tptr.begin(), tptr.end() - 1);
+    for (int64_t i = 0; i < nrows; ++i)
+      for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) {
+        const int64_t d = pos[(size_t)indices[k]]++;
+        tidx[(size_t)d] = i;
+        for (int j = 0; j < nplanes; ++j) tval[(size_t)j * nnz + d] = planes[j][k];
+      }
+    std::vector<const double*> tpl((size_t)nplanes);
+    for (int j = 0; j < nplanes; ++j) tpl[(size_t)j] = tval.data() + (size_t)j * nnz;
+    int rct = mpsg_csr_upload_ex(ctx, K, flags & ~MPSG_CSR_TRANSPOSE, ncols, nrows, tptr.data(), tidx.data(),
+                                 tpl.data(), &A->trans);
+    if (rct) return rct;
+  }
   *out = holder.release();
   return MPSG_OK;
 }
@@ -442,7 +476,9 @@ int mpsg_csr_get_stats(const mpsg_csr* A, mpsg_csr_stats* o) {
   o->nlong = A->nlong;
   o->long_nnz = A->long_nnz;
   o->nchunks = A->nchunks;
-  o->device_bytes = A->device_bytes;
+  o->device_bytes = A->device_bytes + (A->trans ? A->trans->device_bytes : 0);
+  o->is_mixed = A->mixed;
+  o->has_transpose = A->trans != nullptr;
   return MPSG_OK;
 }
 
@@ -494,6 +530,95 @@ int mpsg_spmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen,
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[1], x_im, xb, cudaMemcpyHostToDevice, st));
   }
   if ((rc = launch_spmv(ctx, A, order, ctx->dbuf[0], ctx->dbuf[1], ctx->dbuf[2], ctx->dbuf[3], st))) return rc;
+  if (yb) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(y_re, ctx->dbuf[2], yb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(y_im, ctx->dbuf[3], yb, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MPSG_OK;
+}
+
+// ---- transposed products ----------------------------------------------
+namespace {
+int trans_of(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_csr** T) {
+  if (!A->trans)
+    return fail(ctx, MPSG_E_ARG, "sptmv: matrix was uploaded without MPSG_CSR_TRANSPOSE");
+  *T = A->trans;
+  return MPSG_OK;
+}
+// Exact orders: the reference sptmv at one thread accumulates y[j] over i
+// ascending whether lanes are on or off (SptRow lanes are per-element exact,
+// kernels.hpp:227-322), i.e. the lanes-off row sum of A^T.
+int torder(int order) { return order == MPSG_ORDER_FAST ? MPSG_ORDER_FAST : MPSG_ORDER_SCALAR; }
+}  // namespace
+
+int mpsg_sptmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_v, double* d_y, void* stream) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "sptmv: matrix is complex, use mpsg_sptmv_complex");
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "sptmv: unknown order %d", order);
+  const mpsg_csr* T;
+  int rc = trans_of(ctx, A, &T);
+  if (rc) return rc;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return launch_spmv(ctx, T, torder(order), d_v, nullptr, d_y, nullptr, st);
+}
+
+int mpsg_sptmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t vlen, const double* v, double* y) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (vlen != A->nrows) return fail(ctx, MPSG_E_DIM, "%s", dim_msg("sptmv", vlen, A->nrows).c_str());
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "sptmv: matrix is complex, use mpsg_sptmv_complex");
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "sptmv: unknown order %d", order);
+  const mpsg_csr* T;
+  int rc = trans_of(ctx, A, &T);
+  if (rc) return rc;
+  const size_t vb = (size_t)A->nrows * A->K * sizeof(double), yb = (size_t)A->ncols * A->K * sizeof(double);
+  if ((rc = ensure_scratch(ctx, 0, vb))) return rc;
+  if ((rc = ensure_scratch(ctx, 1, yb))) return rc;
+  cudaStream_t st = ctx->stream;
+  if (vb) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], v, vb, cudaMemcpyHostToDevice, st));
+  if (yb && T->nnz == 0) CUDA_TRY(ctx, cudaMemsetAsync(ctx->dbuf[1], 0, yb, st));
+  if ((rc = launch_spmv(ctx, T, torder(order), ctx->dbuf[0], nullptr, ctx->dbuf[1], nullptr, st))) return rc;
+  if (yb) CUDA_TRY(ctx, cudaMemcpyAsync(y, ctx->dbuf[1], yb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MPSG_OK;
+}
+
+int mpsg_sptmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugate, const double* d_v_re,
+                           const double* d_v_im, double* d_y_re, double* d_y_im, void* stream) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (!A->cplx) return fail(ctx, MPSG_E_ARG, "sptmv_complex: matrix is real");
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "sptmv: unknown order %d", order);
+  const mpsg_csr* T;
+  int rc = trans_of(ctx, A, &T);
+  if (rc) return rc;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return launch_spmv(ctx, T, torder(order), d_v_re, d_v_im, d_y_re, d_y_im, st, conjugate != 0);
+}
+
+int mpsg_sptmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugate, int64_t vlen,
+                       const double* v_re, const double* v_im, double* y_re, double* y_im) {
+  if (!ctx || !A) return MPSG_E_ARG;
+  if (!A->cplx) return fail(ctx, MPSG_E_ARG, "sptmv_complex: matrix is real");
+  if (vlen != A->nrows) return fail(ctx, MPSG_E_DIM, "%s", dim_msg("sptmv", vlen, A->nrows).c_str());
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "sptmv: unknown order %d", order);
+  const mpsg_csr* T;
+  int rc = trans_of(ctx, A, &T);
+  if (rc) return rc;
+  const size_t vb = (size_t)A->nrows * A->K * sizeof(double), yb = (size_t)A->ncols * A->K * sizeof(double);
+  for (int sl = 0; sl < 4; ++sl)
+    if ((rc = ensure_scratch(ctx, sl, sl < 2 ? vb : yb))) return rc;
+  cudaStream_t st = ctx->stream;
+  if (vb) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], v_re, vb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[1], v_im, vb, cudaMemcpyHostToDevice, st));
+  }
+  if (yb && T->nnz == 0) {
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->dbuf[2], 0, yb, st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->dbuf[3], 0, yb, st));
+  }
+  if ((rc = launch_spmv(ctx, T, torder(order), ctx->dbuf[0], ctx->dbuf[1], ctx->dbuf[2], ctx->dbuf[3], st,
+                        conjugate != 0)))
+    return rc;
   if (yb) {
     CUDA_TRY(ctx, cudaMemcpyAsync(y_re, ctx->dbuf[2], yb, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(ctx, cudaMemcpyAsync(y_im, ctx->dbuf[3], yb, cudaMemcpyDeviceToHost, st));

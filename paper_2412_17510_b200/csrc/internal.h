@@ -41,6 +41,8 @@ struct mpsg_ctx {
 struct mpsg_csr {
   int K = 2;
   bool cplx = false;
+  bool mixed = false;         // binary64 values (Mixed mode, kernels.hpp:55-58)
+  mpsg_csr* trans = nullptr;  // device transpose, for the transposed products
   int64_t nrows = 0, ncols = 0, nnz = 0;
   // SELL store
   int C = 32;
@@ -123,10 +125,11 @@ cudaError_t launch_win(const mpsg_ctx* ctx, void (*kern)(KArgs...), dim3 grid, d
 // SpMV launch for one (K, complex) instantiation (spmv_k{2,3,4}.cu).
 template <int K, bool CPLX>
 int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre,
-                  const double* xim, double* yre, double* yim, cudaStream_t st);
-// Dispatch over K / complex (capi.cu).
+                  const double* xim, double* yre, double* yim, cudaStream_t st, bool conj);
+// Dispatch over K / complex (capi.cu).  conj: complex combine of the adjoint
+// (y.re = rr + ii, y.im = ri - ir).
 int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
-                double* yre, double* yim, cudaStream_t st);
+                double* yre, double* yim, cudaStream_t st, bool conj = false);
 // Device CG driver for one K (cg_k{2,3,4}.cu).
 template <int K>
 int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, const double* x0,

@@ -3,18 +3,17 @@
 #include "internal.h"
 #include "spmv_kernels.cuh"
 
-#ifndef MPSG_FAST_COMPLEX_ORDER
-#define MPSG_FAST_COMPLEX_ORDER ORDER_SCALAR
-#endif
-
 namespace mpsg {
 
-template <int K, bool CPLX>
-int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre,
-                  const double* xim, double* yre, double* yim, cudaStream_t st) {
+// Launch every kernel of one SpMV over the device layout of A (layout.h):
+// the long-row kernel on the context's aux stream (forked/joined by events)
+// concurrently with the SELL kernel on `st`.
+template <int K, bool CPLX, bool MX, bool CONJ>
+int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
+                     double* yre, double* yim, cudaStream_t st) {
   const bool has_long = A->nlong > 0;
   // x (re, then im for complex: one window over the first, the hotter, is
-  // all a launch can carry) stays L2-resident while the matrix streams
+  // all a launch can carry) -- see launch_win; off unless MPSG_L2_PERSIST=1
   const size_t xb = (size_t)A->ncols * K * sizeof(double);
   if (has_long) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));
@@ -22,15 +21,17 @@ int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre
     LongView L = A->lng();
     if (order == ORDER_FAST) {
       const int blocks = (int)((A->nchunks + 3) / 4);
-      CUDA_TRY(ctx, launch_win(ctx, long_fast_kernel<K, CPLX>, blocks, 128, 0, ctx->aux, xre, xb, L, xre, xim,
-                               yre, yim));
+      CUDA_TRY(ctx, launch_win(ctx, long_fast_kernel<K, CPLX, MX, CONJ>, blocks, 128, 0, ctx->aux, xre, xb, L, xre,
+                               xim, yre, yim));
     } else {
       constexpr int CH = CPLX ? 256 : 512;
       const size_t smem = (size_t)CH * (CPLX ? 4 : 1) * sizeof(MC<K>);
       if (order == ORDER_SCALAR)
-        long_det_kernel<K, ORDER_SCALAR, CPLX, CH><<<(int)A->nlong, 128, smem, ctx->aux>>>(L, xre, xim, yre, yim);
+        long_det_kernel<K, ORDER_SCALAR, CPLX, CH, MX, CONJ>
+            <<<(int)A->nlong, 128, smem, ctx->aux>>>(L, xre, xim, yre, yim);
       else
-        long_det_kernel<K, ORDER_LANE4, CPLX, CH><<<(int)A->nlong, 128, smem, ctx->aux>>>(L, xre, xim, yre, yim);
+        long_det_kernel<K, ORDER_LANE4, CPLX, CH, MX, CONJ>
+            <<<(int)A->nlong, 128, smem, ctx->aux>>>(L, xre, xim, yre, yim);
     }
     CUDA_TRY(ctx, cudaGetLastError());
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));
@@ -45,19 +46,20 @@ int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre
     const int sorder = order == ORDER_FAST ? ORDER_SCALAR : order;
     if constexpr (!CPLX) {
       if (sorder == ORDER_SCALAR)
-        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_SCALAR>, blocks, 128, 0, st, xre, xb, S, xre, yre));
+        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_SCALAR, MX>, blocks, 128, 0, st, xre, xb, S, xre,
+                                 yre));
       else if constexpr (K == 2)
-        CUDA_TRY(ctx, launch_win(ctx, sell_real_lane4_lat_kernel<K>, blocks, 128, 0, st, xre, xb, S, xre, yre));
+        CUDA_TRY(ctx, launch_win(ctx, sell_real_lane4_lat_kernel<K, MX>, blocks, 128, 0, st, xre, xb, S, xre, yre));
       else
-        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_LANE4>, blocks, 128, 0, st, xre, xb, S, xre, yre));
+        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_LANE4, MX>, blocks, 128, 0, st, xre, xb, S, xre,
+                                 yre));
     } else {
-      const int corder = order == ORDER_FAST ? MPSG_FAST_COMPLEX_ORDER : order;
-      if (corder == ORDER_SCALAR)
-        CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_SCALAR>, blocks, 128, 0, st, xre, xb, S, xre,
-                                 xim, yre, yim));
+      if (sorder == ORDER_SCALAR)
+        CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_SCALAR, MX, CONJ>, blocks, 128, 0, st, xre, xb,
+                                 S, xre, xim, yre, yim));
       else
-        CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_LANE4>, blocks, 128, 0, st, xre, xb, S, xre,
-                                 xim, yre, yim));
+        CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_LANE4, MX, CONJ>, blocks, 128, 0, st, xre, xb,
+                                 S, xre, xim, yre, yim));
     }
     CUDA_TRY(ctx, cudaGetLastError());
   }
@@ -65,11 +67,25 @@ int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre
   return MPSG_OK;
 }
 
+template <int K, bool CPLX>
+int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
+                  double* yre, double* yim, cudaStream_t st, bool conj) {
+  if constexpr (CPLX) {
+    if (A->mixed)
+      return conj ? launch_spmv_mode<K, true, true, true>(ctx, A, order, xre, xim, yre, yim, st)
+                  : launch_spmv_mode<K, true, true, false>(ctx, A, order, xre, xim, yre, yim, st);
+    return conj ? launch_spmv_mode<K, true, false, true>(ctx, A, order, xre, xim, yre, yim, st)
+                : launch_spmv_mode<K, true, false, false>(ctx, A, order, xre, xim, yre, yim, st);
+  } else {
+    if (A->mixed) return launch_spmv_mode<K, false, true, false>(ctx, A, order, xre, xim, yre, yim, st);
+    return launch_spmv_mode<K, false, false, false>(ctx, A, order, xre, xim, yre, yim, st);
+  }
+}
 
 }  // namespace mpsg
 
-#define MPSG_INSTANTIATE_SPMV(K)                                                              \
-  template int mpsg::launch_spmv_k<K, false>(mpsg_ctx*, const mpsg_csr*, int, const double*,   \
-                                             const double*, double*, double*, cudaStream_t);   \
-  template int mpsg::launch_spmv_k<K, true>(mpsg_ctx*, const mpsg_csr*, int, const double*,    \
-                                            const double*, double*, double*, cudaStream_t);
+#define MPSG_INSTANTIATE_SPMV(K)                                                                            \
+  template int mpsg::launch_spmv_k<K, false>(mpsg_ctx*, const mpsg_csr*, int, const double*, const double*, \
+                                             double*, double*, cudaStream_t, bool);                          \
+  template int mpsg::launch_spmv_k<K, true>(mpsg_ctx*, const mpsg_csr*, int, const double*, const double*,  \
+                                            double*, double*, cudaStream_t, bool);

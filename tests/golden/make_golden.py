@@ -188,13 +188,39 @@ def cg_full():
     return out
 
 
+def mixed_sptmv():
+    """Mixed-mode SpMV and (complex) sptmv outputs from the real reference."""
+    from tests.util import mixed_of
+
+    cases = {"cfg2": (2, 600, 32.0, 0.0), "cfg4": (4, 3000, 700.0, 1.8)}
+    out = {}
+    for name, K, order in (("cfg2", 4, 1), ("cfg4", 2, 0)):
+        c = cases[name]
+        A = mixed_of(synth.config_matrix(c[0], K, *c[1:]))
+        x = synth.config_vector(c[0], A.nrows, K)
+        out[f"mixed_{name}_K{K}_o{order}"] = O.ref_spmv(A, x, order, mixed=True)
+    for name, K, mixed in (("cfg2", 3, False), ("cfg4", 2, True)):
+        c = cases[name]
+        A = synth.config_matrix(c[0], K, *c[1:])
+        if mixed:
+            A = mixed_of(A)
+        v = synth.config_vector(c[0], A.nrows, K)
+        out[f"sptmv_{'mixed_' if mixed else ''}{name}_K{K}"] = O.ref_sptmv(A, v, 1, threads=1, mixed=mixed)
+    A = synth.config_matrix(3, 4, 300, 24.0)
+    vr, vi = synth.config_vector(3, A.nrows, 4)
+    yr, yi = O.ref_sptmv_complex(A, vr, vi, 1, threads=1, conjugate=True)
+    out["csptmv_K4_conj_re"], out["csptmv_K4_conj_im"] = yr, yi
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cg-full", action="store_true")
     ap.add_argument("--only", default="")
     a = ap.parse_args()
     assert O.ref_available(), "build the reference first: make -C oracle ref"
-    jobs = {"arith": arith, "spmv_small": spmv_small, "spmv_full": spmv_full, "cg_small": cg_small}
+    jobs = {"arith": arith, "spmv_small": spmv_small, "spmv_full": spmv_full, "cg_small": cg_small,
+            "mixed_sptmv": mixed_sptmv}
     if a.cg_full:
         jobs = {"cg_full": cg_full}
     for name, fn in jobs.items():

@@ -176,3 +176,55 @@ def test_live_reference_random_matrices(K):
     x = synth.vector(synth.VAL_NORMAL, 300, K, seed=5)
     for order in (0, 1):
         assert bits_equal(O.spmv(A, x, order), O.ref_spmv(A, x, order))
+
+
+# ---- Mixed mode and transposed products ----------------
+from tests.util import mixed_of  # noqa: E402
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_mixed_and_sptmv_match_live_reference(K):
+    if not O.ref_available():
+        pytest.skip("reference not built here")
+    A = synth.config_matrix(4, K, 1500, 400.0, 1.8)
+    x = synth.config_vector(4, A.nrows, K)
+    Am = mixed_of(A)
+    for order in (0, 1):
+        assert O.spmv(Am, x, order, mixed=True).tobytes() == O.ref_spmv(Am, x, order, mixed=True).tobytes()
+        for threads in (1, 2, 5):
+            # sptmv: lanes on/off give the same bits; thread count changes the merge order
+            assert O.sptmv(A, x, threads).tobytes() == O.ref_sptmv(A, x, order, threads=threads).tobytes()
+            assert (O.sptmv(Am, x, threads, mixed=True).tobytes() ==
+                    O.ref_sptmv(Am, x, order, threads=threads, mixed=True).tobytes())
+    C = synth.config_matrix(3, K, 150, 10.0)
+    xr, xi = synth.config_vector(3, C.nrows, K)
+    for mixed, MM in ((False, C), (True, mixed_of(C, cplx=True))):
+        a = O.spmv_complex(MM, xr, xi, 1, mixed=mixed)
+        b = O.ref_spmv_complex(MM, xr, xi, 1, mixed=mixed)
+        assert all(p.tobytes() == q.tobytes() for p, q in zip(a, b))
+        for conj in (False, True):
+            a = O.sptmv_complex(MM, xr, xi, 1, conj, mixed)
+            b = O.ref_sptmv_complex(MM, xr, xi, 0, 1, conj, mixed)
+            assert all(p.tobytes() == q.tobytes() for p, q in zip(a, b))
+
+
+def test_mixed_sptmv_goldens_pin_the_oracle():
+    g = golden("mixed_sptmv")
+    c = {"cfg2": (2, 600, 32.0, 0.0), "cfg4": (4, 3000, 700.0, 1.8)}
+    A = mixed_of(synth.config_matrix(2, 4, *c["cfg2"][1:]))
+    assert O.spmv(A, synth.config_vector(2, A.nrows, 4), 1, mixed=True).tobytes() == g["mixed_cfg2_K4_o1"].tobytes()
+    A = synth.config_matrix(2, 3, *c["cfg2"][1:])
+    assert O.sptmv(A, synth.config_vector(2, A.nrows, 3)).tobytes() == g["sptmv_cfg2_K3"].tobytes()
+    A = synth.config_matrix(3, 4, 300, 24.0)
+    vr, vi = synth.config_vector(3, A.nrows, 4)
+    yr, yi = O.sptmv_complex(A, vr, vi, 1, True)
+    assert yr.tobytes() == g["csptmv_K4_conj_re"].tobytes() and yi.tobytes() == g["csptmv_K4_conj_im"].tobytes()
+
+
+def test_sptmv_single_thread_equals_spmv_of_transpose():
+    # test_kernels.cpp:152-174 / acceptance check 6: sptmv(1 thread, lanes off) == spmv(A^T)
+    from tests.util import transpose
+
+    A = synth.config_matrix(2, 2, 700, 16.0)
+    v = synth.config_vector(2, A.nrows, 2)
+    assert O.sptmv(A, v).tobytes() == O.spmv(transpose(A), v, 0).tobytes()

@@ -82,3 +82,25 @@ def bound_ok(A, x, y, yref, K, extra=None):
     with np.errstate(divide="ignore", invalid="ignore"):
         ratio = np.where(lim > 0, d / lim, np.where(d == 0, 0.0, np.inf))
     return bool(np.all(d <= lim)), float(np.max(ratio)) if len(ratio) else 0.0
+
+
+def mixed_of(A, cplx=False):
+    """The binary64 matrix of Mixed mode: the leading plane (re, im for complex)."""
+    K = A.K
+    planes = np.stack([A.planes[0], A.planes[K]]) if cplx else A.planes[:1].copy()
+    return SimpleNamespace(nrows=A.nrows, ncols=A.ncols, indptr=A.indptr, indices=A.indices,
+                           planes=np.ascontiguousarray(planes), K=K, nnz=A.nnz)
+
+
+def transpose(A):
+    """Host A^T with rows listing entries in ascending original row (transpose_csr, sparse.hpp:139-163)."""
+    indptr = np.asarray(A.indptr, np.int64)
+    rows = np.repeat(np.arange(A.nrows, dtype=np.int64), np.diff(indptr))
+    cols = np.asarray(A.indices, np.int64)
+    perm = np.lexsort((rows, cols))
+    tptr = np.zeros(A.ncols + 1, np.int64)
+    np.add.at(tptr, cols + 1, 1)
+    tptr = np.cumsum(tptr)
+    planes = np.ascontiguousarray(np.asarray(A.planes)[:, perm])
+    return SimpleNamespace(nrows=A.ncols, ncols=A.nrows, indptr=tptr, indices=rows[perm], planes=planes,
+                           K=getattr(A, "K", None), nnz=len(perm))
