@@ -1,4 +1,4 @@
-// mps/gpu.hpp -- C++ drop-in for the reference's SpMV / CG path on B200.
+// mps/gpu.hpp -- C++ drop-in for the reference's SpMV / SpTMV / CG path on B200.
 //
 // Header-only layer over the C ABI in mpsg.h (libmpsg.so).  It takes and
 // returns the reference's own types, so a caller of the reference
@@ -8,34 +8,42 @@
 //   -----------------------------------------------------  -----------------------------------
 //   mps::spmv(const CsrMatrix<E>&, const std::vector<F>&,  mps::gpu::spmv (same signature)
 //             const KernelMode&)        kernels.hpp:348
+//   mps::sptmv(...)                     kernels.hpp:368    mps::gpu::sptmv (same signature)
 //   mps::spmv_complex(const ComplexSparseMatrix<E>&,       mps::gpu::spmv_complex (same)
 //             const ComplexVector<F>&, const KernelMode&)  kernels.hpp:399
+//   mps::sptmv_complex(..., bool conjugate) kernels.hpp:419 mps::gpu::sptmv_complex (same)
 //   mps::CsrOperator<E> (Op concept)    krylov.hpp:101     mps::gpu::GpuCsrOperator<E>
 //   mps::solve_cg(op, b, cfg)           krylov.hpp:238     mps::gpu::solve_cg (device-resident)
-//                                                          -- or the reference solve_cg itself
-//                                                          with a GpuCsrOperator (same Op concept)
+//                                                          -- or the reference's own solvers
+//                                                          (solve_cg, solve_bicg, ...) with a
+//                                                          GpuCsrOperator (same Op concept)
 //   mps::detail::partition_rows         kernels.hpp:63     mps::gpu::partition_rows
 //   mps::checksum                       bench.hpp:113      (unchanged; results are host vectors)
+//
+// Element types (kernels.hpp:50-60): Pure mode, E = F = MultiComponent<K>
+// (K = 2, 3, 4); Mixed mode, E = double and F = MultiComponent<K> (the
+// paper's "M": binary64 matrix, product mul_by_double(v, a)).  Other types
+// (binary64 x binary64, BigFloat) fail to compile: there is no CPU fallback.
 //
 // Include the reference headers first (this file uses mps::CsrMatrix,
 // MultiComponent, KernelMode, SolverConfig, SolveResult, ...), then this one;
 // link libmpsg.so.  Semantics kept from the reference:
 //  * KernelMode::lanes_enabled selects the accumulation order, reproduced bit
-//    for bit (true: row_sum_lanes_pure, kernels.hpp:103; false:
+//    for bit (true: row_sum_lanes_*, kernels.hpp:103-142; false:
 //    row_sum_scalar, kernels.hpp:90).  KernelMode::threads has no device
-//    meaning and is ignored.  The overloads taking mps::gpu::Order::Fast
-//    select the throughput order (componentwise error bound instead of bits).
+//    meaning for spmv and is ignored; sptmv reproduces the reference at one
+//    thread (lanes do not change its bits).  The overloads taking
+//    mps::gpu::Order::Fast select the throughput order (componentwise error
+//    bound instead of bits).
 //  * dimension errors throw std::invalid_argument with the reference message
 //    (kernels.hpp:333-339); solver breakdown / divergence are reported in
 //    SolverReport, never thrown (krylov.hpp:46, 203-213).
 //  * host-vector calls are synchronous, like the reference.
-// Only the Pure matrix mode (matrix and vector in the same MultiComponent<K>,
-// K = 2, 3, 4) runs on the device; other element types fail to compile
-// (there is no CPU fallback).
 //
-// Matrices are uploaded once and cached by address (+ a structural
-// fingerprint).  A caller that rewrites a matrix's values in place between
-// calls must call mps::gpu::invalidate(A) (or hold an explicit DeviceCsr).
+// The reference-signature drop-ins upload a matrix once and cache it by
+// address (+ a structural fingerprint).  A caller that rewrites a matrix's
+// values in place between calls must call mps::gpu::invalidate(A) (or hold
+// an explicit DeviceCsr).
 #pragma once
 
 #include <cstdint>
@@ -60,12 +68,32 @@ struct mc_width : std::integral_constant<int, 0> {};
 template <int K>
 struct mc_width<MultiComponent<K>> : std::integral_constant<int, K> {};
 
+// (matrix element, vector element) pairs the device runs
+template <class E, class F>
+struct device_pair : std::false_type {};
+template <int K>
+struct device_pair<MultiComponent<K>, MultiComponent<K>> : std::true_type {};  // Pure
+template <int K>
+struct device_pair<double, MultiComponent<K>> : std::true_type {};  // Mixed
+
 inline void raise(mpsg_ctx* ctx, int rc) {
   if (rc == MPSG_OK) return;
   std::string msg = mpsg_last_error(ctx);
   if (rc == MPSG_E_DIM) throw std::invalid_argument(msg);
   throw std::runtime_error("mpsg error " + std::to_string(rc) + ": " + msg);
 }
+
+inline std::string dim_msg(const char* what, std::size_t v, std::int64_t m) {  // kernels.hpp:333-339
+  return std::string(what) + ": vector length " + std::to_string(v) + " does not match matrix dimension " +
+         std::to_string(m);
+}
+
+// value planes of one CsrMatrix part: K SoA planes (Pure), or the binary64 array (Mixed)
+template <int K>
+void planes_of(const CsrMatrix<MultiComponent<K>>& A, const double** out) {
+  for (int j = 0; j < K; ++j) out[j] = A.values.component(j);  // sparse.hpp:63
+}
+inline void planes_of(const CsrMatrix<double>& A, const double** out) { out[0] = A.values.data(); }
 }  // namespace detail
 
 // ---------------------------------------------------------------- context
@@ -99,33 +127,31 @@ enum class Order : int { Scalar = MPSG_ORDER_SCALAR, Lane4 = MPSG_ORDER_LANE4, F
 inline Order order_of(const KernelMode& m) { return m.lanes_enabled ? Order::Lane4 : Order::Scalar; }
 
 // ------------------------------------------------------------- matrices
-// Device copy of a CsrMatrix<MultiComponent<K>> or of a
-// ComplexSparseMatrix<MultiComponent<K>> (one shared structure).
-template <class E>
+// Device copy of a CsrMatrix<E> or ComplexSparseMatrix<E> (one shared
+// structure) for vectors of F; with_transpose also uploads A^T for sptmv.
+template <class E, class F = E>
 class DeviceCsr {
-  static constexpr int K = detail::mc_width<E>::value;
-  static_assert(K >= 2, "mps::gpu: device matrices hold MultiComponent<2|3|4> values (Pure mode)");
+  static_assert(detail::device_pair<E, F>::value,
+                "mps::gpu: the device runs MultiComponent<K> x MultiComponent<K> (Pure) and "
+                "double x MultiComponent<K> (Mixed) products");
 
  public:
-  DeviceCsr(const CsrMatrix<E>& A, Context& ctx = Context::instance()) : ctx_(&ctx) {
-    const double* planes[K];
-    for (int j = 0; j < K; ++j) planes[j] = A.values.component(j);
-    ctx.check(mpsg_csr_upload(ctx.get(), K, 0, A.nrows, A.ncols, A.indptr.data(), A.indices.data(), planes,
-                              &h_));
-    nrows_ = A.nrows;
-    ncols_ = A.ncols;
+  static constexpr int K = detail::mc_width<F>::value;
+  static constexpr bool kMixed = std::is_same<E, double>::value;
+  static constexpr int kPlanes = kMixed ? 1 : K;
+
+  DeviceCsr(const CsrMatrix<E>& A, bool with_transpose = false, Context& ctx = Context::instance()) : ctx_(&ctx) {
+    const double* planes[kPlanes];
+    detail::planes_of(A, planes);
+    upload(A, 0, planes, with_transpose);
   }
-  DeviceCsr(const ComplexSparseMatrix<E>& A, Context& ctx = Context::instance()) : ctx_(&ctx) {
+  DeviceCsr(const ComplexSparseMatrix<E>& A, bool with_transpose = false, Context& ctx = Context::instance())
+      : ctx_(&ctx) {
     check_split_structure(A);  // sparse.hpp:254-259
-    const double* planes[2 * K];
-    for (int j = 0; j < K; ++j) {
-      planes[j] = A.re.values.component(j);
-      planes[K + j] = A.im.values.component(j);
-    }
-    ctx.check(mpsg_csr_upload(ctx.get(), K, 1, A.re.nrows, A.re.ncols, A.re.indptr.data(), A.re.indices.data(),
-                              planes, &h_));
-    nrows_ = A.re.nrows;
-    ncols_ = A.re.ncols;
+    const double* planes[2 * kPlanes];
+    detail::planes_of(A.re, planes);
+    detail::planes_of(A.im, planes + kPlanes);
+    upload(A.re, MPSG_CSR_COMPLEX, planes, with_transpose);
   }
   ~DeviceCsr() { mpsg_csr_destroy(h_); }
   DeviceCsr(const DeviceCsr&) = delete;
@@ -133,33 +159,55 @@ class DeviceCsr {
 
   std::int64_t rows() const { return nrows_; }
   std::int64_t cols() const { return ncols_; }
+  bool has_transpose() const { return trans_; }
   const mpsg_csr* get() const { return h_; }
   Context& context() const { return *ctx_; }
 
  private:
+  void upload(const CsrMatrix<E>& S, int flags, const double* const* planes, bool with_transpose) {
+    flags |= (kMixed ? MPSG_CSR_MIXED : 0) | (with_transpose ? MPSG_CSR_TRANSPOSE : 0);
+    ctx_->check(mpsg_csr_upload_ex(ctx_->get(), K, flags, S.nrows, S.ncols, S.indptr.data(), S.indices.data(),
+                                   planes, &h_));
+    nrows_ = S.nrows;
+    ncols_ = S.ncols;
+    trans_ = with_transpose;
+  }
   Context* ctx_;
   mpsg_csr* h_ = nullptr;
   std::int64_t nrows_ = 0, ncols_ = 0;
+  bool trans_ = false;
 };
 
-template <class E>
-std::vector<E> spmv(const DeviceCsr<E>& A, const std::vector<E>& v, Order order) {
-  std::vector<E> y(static_cast<std::size_t>(A.rows()));
-  static_assert(sizeof(E) == sizeof(double) * detail::mc_width<E>::value, "MultiComponent must be K doubles");
+template <class E, class F>
+std::vector<F> spmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, Order order) {
+  static_assert(sizeof(F) == sizeof(double) * detail::mc_width<F>::value, "MultiComponent must be K doubles");
+  std::vector<F> y(static_cast<std::size_t>(A.rows()));
   A.context().check(mpsg_spmv(A.context().get(), A.get(), static_cast<int>(order), static_cast<std::int64_t>(v.size()),
                               reinterpret_cast<const double*>(v.data()), reinterpret_cast<double*>(y.data())));
   return y;
 }
-
-template <class E>
-std::vector<E> spmv(const DeviceCsr<E>& A, const std::vector<E>& v, const KernelMode& mode) {
+template <class E, class F>
+std::vector<F> spmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, const KernelMode& mode) {
   return spmv(A, v, order_of(mode));
 }
 
-template <class E>
-ComplexVector<E> spmv_complex(const DeviceCsr<E>& A, const ComplexVector<E>& v, Order order) {
+template <class E, class F>
+std::vector<F> sptmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, Order order) {
+  std::vector<F> y(static_cast<std::size_t>(A.cols()));
+  A.context().check(mpsg_sptmv(A.context().get(), A.get(), static_cast<int>(order),
+                               static_cast<std::int64_t>(v.size()), reinterpret_cast<const double*>(v.data()),
+                               reinterpret_cast<double*>(y.data())));
+  return y;
+}
+template <class E, class F>
+std::vector<F> sptmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, const KernelMode& mode) {
+  return sptmv(A, v, order_of(mode));
+}
+
+template <class E, class F>
+ComplexVector<F> spmv_complex(const DeviceCsr<E, F>& A, const ComplexVector<F>& v, Order order) {
   if (v.re.size() != v.im.size()) throw std::invalid_argument("spmv_complex: re/im vector length mismatch");
-  ComplexVector<E> y;
+  ComplexVector<F> y;
   y.re.resize(static_cast<std::size_t>(A.rows()));
   y.im.resize(static_cast<std::size_t>(A.rows()));
   A.context().check(mpsg_spmv_complex(A.context().get(), A.get(), static_cast<int>(order),
@@ -170,10 +218,25 @@ ComplexVector<E> spmv_complex(const DeviceCsr<E>& A, const ComplexVector<E>& v, 
                                       reinterpret_cast<double*>(y.im.data())));
   return y;
 }
-
-template <class E>
-ComplexVector<E> spmv_complex(const DeviceCsr<E>& A, const ComplexVector<E>& v, const KernelMode& mode) {
+template <class E, class F>
+ComplexVector<F> spmv_complex(const DeviceCsr<E, F>& A, const ComplexVector<F>& v, const KernelMode& mode) {
   return spmv_complex(A, v, order_of(mode));
+}
+
+template <class E, class F>
+ComplexVector<F> sptmv_complex(const DeviceCsr<E, F>& A, const ComplexVector<F>& v, Order order,
+                               bool conjugate = false) {
+  if (v.re.size() != v.im.size()) throw std::invalid_argument("sptmv_complex: re/im vector length mismatch");
+  ComplexVector<F> y;
+  y.re.resize(static_cast<std::size_t>(A.cols()));
+  y.im.resize(static_cast<std::size_t>(A.cols()));
+  A.context().check(mpsg_sptmv_complex(A.context().get(), A.get(), static_cast<int>(order), conjugate ? 1 : 0,
+                                       static_cast<std::int64_t>(v.re.size()),
+                                       reinterpret_cast<const double*>(v.re.data()),
+                                       reinterpret_cast<const double*>(v.im.data()),
+                                       reinterpret_cast<double*>(y.re.data()),
+                                       reinterpret_cast<double*>(y.im.data())));
+  return y;
 }
 
 // --------------------------------------------------- upload cache (drop-in)
@@ -187,64 +250,90 @@ struct CacheKey {
     return std::tie(addr, indptr, plane0, nnz) < std::tie(o.addr, o.indptr, o.plane0, o.nnz);
   }
 };
-template <class E>
-std::map<CacheKey, std::shared_ptr<DeviceCsr<E>>>& cache() {
-  static std::map<CacheKey, std::shared_ptr<DeviceCsr<E>>> c;
+template <class E, class F>
+std::map<CacheKey, std::shared_ptr<DeviceCsr<E, F>>>& cache() {
+  static std::map<CacheKey, std::shared_ptr<DeviceCsr<E, F>>> c;
   return c;
 }
 template <class E>
 CacheKey key_of(const CsrMatrix<E>& A) {
-  return {&A, A.indptr.data(), A.values.component(0), A.nnz()};
+  const double* p[16];
+  planes_of(A, p);
+  return {&A, A.indptr.data(), p[0], A.nnz()};
 }
 template <class E>
 CacheKey key_of(const ComplexSparseMatrix<E>& A) {
-  return {&A, A.re.indptr.data(), A.re.values.component(0), A.re.nnz()};
+  const double* p[16];
+  planes_of(A.re, p);
+  return {&A, A.re.indptr.data(), p[0], A.re.nnz()};
 }
-template <class E, class M>
-const DeviceCsr<E>& cached(const M& A) {
-  auto& c = cache<E>();
+template <class E, class F, class M>
+const DeviceCsr<E, F>& cached(const M& A, bool need_transpose) {
+  auto& c = cache<E, F>();
   const CacheKey k = key_of(A);
   auto it = c.find(k);
-  if (it == c.end()) {
-    // drop stale entries for the same address (the matrix was rebuilt)
+  if (it == c.end() || (need_transpose && !it->second->has_transpose())) {
+    // drop stale entries for the same address (rebuilt matrix / no transpose yet)
     for (auto jt = c.begin(); jt != c.end();) jt = (jt->first.addr == k.addr) ? c.erase(jt) : std::next(jt);
-    it = c.emplace(k, std::make_shared<DeviceCsr<E>>(A)).first;
+    it = c.emplace(k, std::make_shared<DeviceCsr<E, F>>(A, need_transpose)).first;
   }
   return *it->second;
+}
+template <class M>
+void invalidate_addr(const M& A) {
+  auto drop = [&](auto& c) {
+    for (auto it = c.begin(); it != c.end();) it = (it->first.addr == &A) ? c.erase(it) : std::next(it);
+  };
+  drop(cache<MultiComponent<2>, MultiComponent<2>>());
+  drop(cache<MultiComponent<3>, MultiComponent<3>>());
+  drop(cache<MultiComponent<4>, MultiComponent<4>>());
+  drop(cache<double, MultiComponent<2>>());
+  drop(cache<double, MultiComponent<3>>());
+  drop(cache<double, MultiComponent<4>>());
 }
 }  // namespace detail
 
 template <class E>
 void invalidate(const CsrMatrix<E>& A) {
-  auto& c = detail::cache<E>();
-  for (auto it = c.begin(); it != c.end();) it = (it->first.addr == &A) ? c.erase(it) : std::next(it);
+  detail::invalidate_addr(A);
 }
 template <class E>
 void invalidate(const ComplexSparseMatrix<E>& A) {
-  auto& c = detail::cache<E>();
-  for (auto it = c.begin(); it != c.end();) it = (it->first.addr == &A) ? c.erase(it) : std::next(it);
+  detail::invalidate_addr(A);
 }
 
 // ---------------------------------------- reference-signature drop-ins
 // mps::spmv (kernels.hpp:348-366)
 template <class E, class F>
 std::vector<F> spmv(const CsrMatrix<E>& A, const std::vector<F>& v, const KernelMode& mode) {
-  static_assert(std::is_same<E, F>::value, "mps::gpu::spmv: only the Pure mode (E == F) runs on the device");
-  if (static_cast<std::size_t>(A.ncols) != v.size())  // kernels.hpp:333-339
-    throw std::invalid_argument("spmv: vector length " + std::to_string(v.size()) +
-                                " does not match matrix dimension " + std::to_string(A.ncols));
-  return spmv(detail::cached<E>(A), v, mode);
+  if (static_cast<std::size_t>(A.ncols) != v.size()) throw std::invalid_argument(detail::dim_msg("spmv", v.size(), A.ncols));
+  return spmv(detail::cached<E, F>(A, false), v, mode);
+}
+
+// mps::sptmv (kernels.hpp:368-394), the reference's one-thread order
+template <class E, class F>
+std::vector<F> sptmv(const CsrMatrix<E>& A, const std::vector<F>& v, const KernelMode& mode) {
+  if (static_cast<std::size_t>(A.nrows) != v.size()) throw std::invalid_argument(detail::dim_msg("sptmv", v.size(), A.nrows));
+  return sptmv(detail::cached<E, F>(A, true), v, mode);
 }
 
 // mps::spmv_complex (kernels.hpp:399-416)
 template <class E, class F>
 ComplexVector<F> spmv_complex(const ComplexSparseMatrix<E>& A, const ComplexVector<F>& v, const KernelMode& mode) {
-  static_assert(std::is_same<E, F>::value, "mps::gpu::spmv_complex: only the Pure mode runs on the device");
   if (v.re.size() != v.im.size()) throw std::invalid_argument("spmv_complex: re/im vector length mismatch");
   if (static_cast<std::size_t>(A.re.ncols) != v.re.size())
-    throw std::invalid_argument("spmv: vector length " + std::to_string(v.re.size()) +
-                                " does not match matrix dimension " + std::to_string(A.re.ncols));
-  return spmv_complex(detail::cached<E>(A), v, mode);
+    throw std::invalid_argument(detail::dim_msg("spmv", v.re.size(), A.re.ncols));
+  return spmv_complex(detail::cached<E, F>(A, false), v, mode);
+}
+
+// mps::sptmv_complex (kernels.hpp:419-441); conjugate = the adjoint
+template <class E, class F>
+ComplexVector<F> sptmv_complex(const ComplexSparseMatrix<E>& A, const ComplexVector<F>& v, const KernelMode& mode,
+                               bool conjugate = false) {
+  if (v.re.size() != v.im.size()) throw std::invalid_argument("sptmv_complex: re/im vector length mismatch");
+  if (static_cast<std::size_t>(A.re.nrows) != v.re.size())
+    throw std::invalid_argument(detail::dim_msg("sptmv", v.re.size(), A.re.nrows));
+  return sptmv_complex(detail::cached<E, F>(A, true), v, order_of(mode), conjugate);
 }
 
 // nnz-balanced contiguous row bounds (kernels.hpp:63-80)
@@ -259,10 +348,11 @@ inline std::vector<std::int64_t> partition_rows(const std::vector<std::int64_t>&
 // ------------------------------------------------------------- solvers
 // The Op concept of krylov.hpp:101-120 over a device-resident matrix: the
 // reference's own solve_cg / solve_bicg / ... run unchanged with it, every
-// apply() being one device SpMV.
-template <class MatE>
+// apply() being one device SpMV and every apply_transposed() one device
+// SpTMV (the matrix must then be uploaded with_transpose).
+template <class MatE, class VecE = MatE>
 struct GpuCsrOperator {
-  const DeviceCsr<MatE>* matrix = nullptr;
+  const DeviceCsr<MatE, VecE>* matrix = nullptr;
   int threads = 1;  // ignored on the device (kept for the reference's shape)
   bool lanes_enabled = true;
   bool fast = false;
@@ -276,18 +366,19 @@ struct GpuCsrOperator {
     return gpu::spmv(*matrix, x, order());
   }
   template <class F>
-  std::vector<F> apply_transposed(const std::vector<F>&) const {
-    throw std::logic_error("mps::gpu::GpuCsrOperator: the transposed product is not on the device yet");
+  std::vector<F> apply_transposed(const std::vector<F>& x) const {
+    return gpu::sptmv(*matrix, x, order());
   }
 };
 
 // Device-resident CG (krylov.hpp:238-281): vectors and scalars never leave
 // the GPU; the residual history, status and true residual come back in the
 // reference's SolverReport.  Only rel_tol, abs_tol, max_iters, x0 and
-// lanes_enabled of SolverConfig are read (as by the reference CG).
+// lanes_enabled of SolverConfig are read (as by the reference CG).  Pure mode.
 template <class E>
-SolveResult<E> solve_cg(const GpuCsrOperator<E>& op, const std::vector<E>& b, const SolverConfig& cfg) {
+SolveResult<E> solve_cg(const GpuCsrOperator<E, E>& op, const std::vector<E>& b, const SolverConfig& cfg) {
   constexpr int K = detail::mc_width<E>::value;
+  static_assert(K >= 2, "device CG runs on MultiComponent<K>");
   cfg.validate();  // krylov.hpp:69-75
   if (op.rows() != op.cols())
     throw std::invalid_argument("solver: operator must be square, got " + std::to_string(op.rows()) + "x" +
@@ -313,7 +404,6 @@ SolveResult<E> solve_cg(const GpuCsrOperator<E>& op, const std::vector<E>& b, co
                     x0.empty() ? nullptr : reinterpret_cast<const double*>(x0.data()), &c,
                     reinterpret_cast<double*>(res.x.data()), hist.data(), static_cast<std::int64_t>(hist.size()),
                     &rep));
-  static_assert(K >= 2, "device CG runs on MultiComponent<K>");
   auto& r = res.report;
   r.status = static_cast<SolverStatus>(rep.status);
   r.converged = rep.converged != 0;

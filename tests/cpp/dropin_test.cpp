@@ -18,7 +18,12 @@
 //  4. the device-resident mps::gpu::solve_cg tracks the reference CG on the
 //     nd3k stand-in (fixtures.hpp:45) and diag(1..40);
 //  5. errors: dimension mismatch throws std::invalid_argument with the
-//     reference's text (kernels.hpp:333-339).
+//     reference's text (kernels.hpp:333-339);
+//  6. Mixed mode (CsrMatrix<double> x MultiComponent<K>, kernels.hpp:55-58)
+//     and the transposed products mps::gpu::sptmv / sptmv_complex (+ adjoint)
+//     bit for bit against the reference at one thread (kernels.hpp:368-441);
+//  7. the reference's own solve_bicg (krylov.hpp:283, uses apply_transposed)
+//     over a GpuCsrOperator: identical history to the host operator.
 #include <bit>
 #include <cmath>
 #include <cstdio>
@@ -197,6 +202,57 @@ void errors() {
   report(!ref_msg.empty() && ref_msg == got_msg, "dimension mismatch message: \"" + got_msg + "\"");
 }
 
+template <int K>
+void mixed_and_transposed(test::Rng& rng) {
+  using E = MultiComponent<K>;
+  auto Ad = coo_to_csr(test::random_coo(rng, 600, 600, 15000));  // binary64 matrix
+  auto v = random_vector<K>(600, rng);
+  for (bool lanes : {true, false}) {
+    KernelMode m{{}, MatrixMode::MixedBinary64, false, 3, lanes};
+    report(same_bits(mps::spmv(Ad, v, m), mps::gpu::spmv(Ad, v, m)),
+           "mixed K=" + std::to_string(K) + (lanes ? " lanes on" : " lanes off") + " spmv bit-exact");
+    KernelMode m1{{}, MatrixMode::MixedBinary64, false, 1, lanes};
+    report(same_bits(mps::sptmv(Ad, v, m1), mps::gpu::sptmv(Ad, v, m1)),
+           "mixed K=" + std::to_string(K) + (lanes ? " lanes on" : " lanes off") + " sptmv bit-exact");
+  }
+  auto A = full_precision<K>(coo_to_csr(test::random_coo(rng, 500, 700, 12000)), rng);
+  auto u = random_vector<K>(500, rng);
+  KernelMode one{{}, MatrixMode::Pure, false, 1, true};
+  report(same_bits(mps::sptmv(A, u, one), mps::gpu::sptmv(A, u, one)),
+         "pure K=" + std::to_string(K) + " sptmv (500x700) bit-exact with the reference at one thread");
+  auto cm = convert_complex_csr<E>(split_complex(test::random_complex_coo(rng, 300, 260, 7000)));
+  for (std::size_t i = 0; i < cm.re.indices.size(); ++i) {
+    cm.re.values.set(i, rng.multicomp<K>(-4, 4));
+    cm.im.values.set(i, rng.multicomp<K>(-4, 4));
+  }
+  ComplexVector<E> cv{random_vector<K>(300, rng), random_vector<K>(300, rng)};
+  for (bool conj : {false, true}) {
+    auto r = mps::sptmv_complex(cm, cv, one, conj);
+    auto g = mps::gpu::sptmv_complex(cm, cv, one, conj);
+    report(same_bits(r.re, g.re) && same_bits(r.im, g.im),
+           "complex K=" + std::to_string(K) + (conj ? " adjoint" : " transpose") + " sptmv_complex bit-exact");
+  }
+}
+
+void bicg_over_gpu_operator() {
+  using E = MultiComponent<2>;
+  test::Rng rng(7);
+  auto A = convert_csr<E>(coo_to_csr(test::random_diag_dominant(rng, 300, 0.05, false)));
+  auto b = make_vector<E>(A.ncols, E(1.0));
+  SolverConfig cfg;
+  cfg.method = KrylovMethod::BiCG;
+  cfg.rel_tol = 1e-25;
+  cfg.max_iters = 200;
+  CsrOperator<E> host_op{&A, 1, true};
+  mps::gpu::DeviceCsr<E> dA(A, /*with_transpose=*/true);
+  mps::gpu::GpuCsrOperator<E> gop{&dA, 1, true};
+  auto ref = mps::solve_bicg(host_op, b, cfg);
+  auto dev = mps::solve_bicg(gop, b, cfg);
+  report(ref.report.residual_history == dev.report.residual_history && same_bits(ref.x, dev.x),
+         "reference solve_bicg over GpuCsrOperator (SpMV + SpTMV on the GPU): identical history (" +
+             std::to_string(ref.report.iterations) + " iterations)");
+}
+
 }  // namespace
 
 int main() {
@@ -211,6 +267,10 @@ int main() {
   solver_suite<4>();
   diag40();
   errors();
+  mixed_and_transposed<2>(rng);
+  mixed_and_transposed<3>(rng);
+  mixed_and_transposed<4>(rng);
+  bicg_over_gpu_operator();
   std::printf("%d failure(s)\n", failures);
   return failures;
 }
