@@ -51,18 +51,21 @@ CONFIG_DESC = {
 # fp64 operations per nonzero for one mul + one add in the reference op
 # sequence (counted with the reference's templated chains)
 OPS_PER_NNZ = {2: 20, 3: 202, 4: 206}
+# Mixed mode (binary64 matrix): one mul_by_double + one add
+OPS_PER_NNZ_MIXED = {2: 17, 3: 130, 4: 152}
 K_NAME = {2: "DD", 3: "TD", 4: "QD"}
 CG_ITERS = 500
 
 
-def algorithmic_bytes(nnz, n, K, cplx):
+def algorithmic_bytes(nnz, n, K, cplx, mixed=False):
     c = 2 if cplx else 1
-    # matrix planes + int32 columns + int32 row pointer + x read once + y written once
-    return nnz * (8 * K * c + 4) + 4 * (n + 1) + 2 * n * 8 * K * c
+    # matrix planes (K, or 1 binary64 plane in mixed mode) + int32 columns +
+    # int32 row pointer + x read once + y written once
+    return nnz * (8 * (1 if mixed else K) * c + 4) + 4 * (n + 1) + 2 * n * 8 * K * c
 
 
-def algorithmic_ops(nnz, K, cplx):
-    return nnz * OPS_PER_NNZ[K] * (4 if cplx else 1)
+def algorithmic_ops(nnz, K, cplx, mixed=False):
+    return nnz * (OPS_PER_NNZ_MIXED if mixed else OPS_PER_NNZ)[K] * (4 if cplx else 1)
 
 
 def cg_iter_bytes(nnz, n, K):
@@ -142,10 +145,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_inputs(cfg: str, K: int):
+def make_inputs(cfg: str, K: int, mixed: bool = False):
     c = int(cfg[3])
     A = synth.config_matrix(c, K)
     x = synth.config_vector(c, A.nrows, K)
+    if mixed:  # the binary64 matrix of Mixed mode: the leading value plane(s)
+        A.planes = np.ascontiguousarray(np.stack([A.planes[0], A.planes[K]]) if c == 3 else A.planes[:1])
     return A, x
 
 
@@ -242,7 +247,8 @@ def max_over_ranks(torch, dev, dist, v):
     return float(t.item())
 
 
-def run_gpu_spmv(args, cfg, K, order, rank, world, dist):
+def run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant="pure"):
+    """variant: "pure" (A in K components), "mixed" (binary64 A), "sptmv" (y = A^T x)."""
     import torch
 
     import paper_2412_17510_b200 as M
@@ -250,9 +256,10 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist):
     dev = torch.device("cuda", torch.cuda.current_device())
     stream, ctx = setup_stream(torch, M, dev)
     cplx = cfg == "cfg3"
-    A, x = make_inputs(cfg, K)
+    mixed, trans = variant == "mixed", variant == "sptmv"
+    A, x = make_inputs(cfg, K, mixed)
     n, nnz = A.nrows, A.nnz
-    shard = args.shard and world > 1
+    shard = args.shard and world > 1 and variant == "pure"
     xs = list(x) if cplx else [x]
     comm = None
     if shard:
@@ -270,12 +277,17 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist):
         local_stats = None
         units = nnz  # strong scaling: the whole matrix per step across the group
     else:
-        dA = M.DeviceCsr(A, K, cplx, ctx=ctx)
+        dA = M.DeviceCsr(A, K, cplx, ctx=ctx, mixed=mixed, transpose=trans)
         local_stats = dA.stats()
         halo = 0
         dxs = [torch.from_numpy(v).to(dev) for v in xs]
         dys = [torch.empty((n, K), dtype=torch.float64, device=dev) for _ in xs]
-        if cplx:
+        if trans and cplx:
+            step = lambda: M.sptmv_complex_dev(dA, dxs[0].data_ptr(), dxs[1].data_ptr(), dys[0].data_ptr(),  # noqa
+                                               dys[1].data_ptr(), order, False, stream.cuda_stream)
+        elif trans:
+            step = lambda: M.sptmv_dev(dA, dxs[0].data_ptr(), dys[0].data_ptr(), order, stream.cuda_stream)  # noqa
+        elif cplx:
             step = lambda: M.spmv_complex_dev(dA, dxs[0].data_ptr(), dxs[1].data_ptr(), dys[0].data_ptr(),  # noqa
                                               dys[1].data_ptr(), order, stream.cuda_stream)
         else:
@@ -307,7 +319,7 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist):
 
     # e2e through the host-pointer C-ABI call (pinned host buffers, H2D + D2H inside)
     e2e = None
-    if not args.no_e2e and not shard:
+    if not args.no_e2e and not shard and variant == "pure":
         if cplx:
             hx = [torch.from_numpy(v).pin_memory() for v in xs]
             hy = [torch.empty((n, K), dtype=torch.float64).pin_memory() for _ in range(2)]
@@ -341,7 +353,7 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist):
     else:
         kernels = 2  # upper bound for a shard (SELL + long-row kernel)
     res = dict(n=n, nnz=nnz, units=units, t_total=t_total, per_launch=t_total / args.steps, clocks=clocks,
-               e2e=e2e, launches=args.steps * kernels, cplx=cplx, halo_rows=halo, shard=shard)
+               e2e=e2e, launches=args.steps * kernels, cplx=cplx, halo_rows=halo, shard=shard, variant=variant)
     del dA
     if comm:
         comm.close()
@@ -409,11 +421,11 @@ def run_gpu_cg(args, K, order, rank, world, dist):
     return out
 
 
-def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey):
+def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey, mixed=False):
     if kind == "cg":
         byts, ops = cg_iter_bytes(nnz, n, K), cg_iter_ops(nnz, n, K)
     else:
-        byts, ops = algorithmic_bytes(nnz, n, K, cplx), algorithmic_ops(nnz, K, cplx)
+        byts, ops = algorithmic_bytes(nnz, n, K, cplx, mixed), algorithmic_ops(nnz, K, cplx, mixed)
     t_hbm, t_fp = byts / (hbm_peak * 1e9), ops / fp64_peak
     if t_hbm >= t_fp:
         ach = byts / seconds / 1e9
@@ -441,6 +453,8 @@ def main():
     ap.add_argument("--order", default="fast", choices=["fast", "lane4", "scalar"])
     ap.add_argument("--shard", action="store_true", help="row-shard the matrix across ranks (configs 3, 4, 5)")
     ap.add_argument("--cg", action="store_true", help="config 5: 500-iteration CG instead of one SpMV")
+    ap.add_argument("--variant", default="pure", choices=["pure", "mixed", "sptmv"],
+                    help="mixed: binary64 matrix (the paper's M mode); sptmv: y = A^T x")
     ap.add_argument("--all", action="store_true", help="one line per config/precision (not the driver line)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -491,28 +505,35 @@ def main():
     fp64_peak = M.measure_fp64_peak(probe)
     probe.close()
 
-    jobs = [(args.config, args.K, args.cg)]
+    jobs = [(args.config, args.K, args.cg, args.variant)]
     if args.all:
-        jobs = [("cfg1", 2, False), ("cfg2", 3, False), ("cfg2", 4, False), ("cfg3", 2, False), ("cfg3", 4, False),
-                ("cfg4", 2, False), ("cfg5", 2, False), ("cfg5", 4, False), ("cfg5", 2, True), ("cfg5", 4, True)]
+        jobs = [("cfg1", 2, False, "pure"), ("cfg2", 3, False, "pure"), ("cfg2", 4, False, "pure"),
+                ("cfg3", 2, False, "pure"), ("cfg3", 4, False, "pure"), ("cfg4", 2, False, "pure"),
+                ("cfg5", 2, False, "pure"), ("cfg5", 4, False, "pure"), ("cfg5", 2, True, "pure"),
+                ("cfg5", 4, True, "pure"), ("cfg2", 4, False, "mixed"), ("cfg4", 2, False, "mixed"),
+                ("cfg3", 4, False, "mixed"), ("cfg2", 4, False, "sptmv"), ("cfg3", 2, False, "sptmv")]
     secondary = None
-    if not args.all and args.config == "cfg2" and args.K == 4 and not args.cg and args.secondary != "none":
-        secondary = ("cfg2", 3, False)
+    if (not args.all and args.config == "cfg2" and args.K == 4 and not args.cg and args.variant == "pure"
+            and args.secondary != "none"):
+        secondary = ("cfg2", 3, False, "pure")
 
     results = []
-    for cfg, K, cg in jobs + ([secondary] if secondary else []):
+    for cfg, K, cg, variant in jobs + ([secondary] if secondary else []):
         if cg:
             r = run_gpu_cg(args, K, order, rank, world, dist)
+            r["variant"] = "pure"
             r["roof"] = roofline("cg", r["nnz"], r["n"], K, False, r["per_iter"], hbm_peak, fp64_peak,
                                  f"cg5_K{K}")
         else:
-            r = run_gpu_spmv(args, cfg, K, order, rank, world, dist)
+            r = run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant)
+            tkey = f"{cfg}_K{K}" + ("" if variant == "pure" else f"_{variant}")
             r["roof"] = roofline("spmv", r["nnz"], r["n"], K, r["cplx"], r["per_launch"], hbm_peak, fp64_peak,
-                                 f"{cfg}_K{K}")
+                                 tkey, mixed=variant == "mixed")
         results.append((cfg, K, cg, r))
 
     if rank == 0:
         for idx, (cfg, K, cg, r) in enumerate(results[: len(jobs)]):
+            vname = {"pure": "", "mixed": " Mixed (binary64 matrix)", "sptmv": " SpTMV y=A^T x"}[r["variant"]]
             steps = 1 if cg else args.steps
             value = r["units"] * steps / r["t_total"] / 1e9
             if r["shard"]:
@@ -525,7 +546,7 @@ def main():
                     "higher_is_better": True, "scaling": "strong" if r["shard"] else "weak",
                     "vs_baseline": None, "dtype": "f64",
                     "data": "synthetic (seeded generators, synth/mpsgen.c)",
-                    "config": {"workload": f"{cfg} {K_NAME[K]}{' CG x500' if cg else ''}: {CONFIG_DESC[cfg]}",
+                    "config": {"workload": f"{cfg} {K_NAME[K]}{' CG x500' if cg else ''}{vname}: {CONFIG_DESC[cfg]}",
                                "precision": K_NAME[K], "order": args.order, "nnz": r["nnz"], "n": r["n"],
                                "parallelism": par,
                                "l2": ("flushed before every timed step: 256 MB write, then 256 MB read of a "
@@ -543,7 +564,7 @@ def main():
                 line["secondary"] = {"workload": f"{c2} {K_NAME[k2]}",
                                      "value": r2["units"] * args.steps / r2["t_total"] / 1e9,
                                      "unit": "Gnnz/s", "roofline": r2["roof"], "e2e": r2["e2e"]}
-            if world == 1 and not args.no_cpu and not args.all:
+            if world == 1 and not args.no_cpu and not args.all and r["variant"] == "pure":
                 cb = run_reference(5 if not cg else 1, 1 if not cg else 0, cfg, K, cg=cg)
                 line["cpu_baseline"] = {"value": cb["value"], "unit": "Gnnz/s", "cores": cb["cores"],
                                         "kind": cb["kind"], "sample": cb["sample"]}

@@ -1,10 +1,9 @@
-# One GPU pass: parity tests, smoke, default bench, all-config bench.
+# One GPU pass: parity tests, smoke, default bench, reference arm, all-config bench.
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
-timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; tail -1 gpurun_out/bench_default.log | cut -c1-600
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-300
-timeout 1200 python bench.py --all --steps 10 --no-e2e > gpurun_out/bench_all.log 2>&1; tail -12 gpurun_out/bench_all.log | cut -c1-250
+timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; tail -1 gpurun_out/bench_default.log | cut -c1-300
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-200
+timeout 1500 python bench.py --all --steps 10 --no-e2e > gpurun_out/bench_all.log 2>&1; tail -2 gpurun_out/bench_all.log | cut -c1-200
