@@ -114,21 +114,71 @@ int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, 
   if (A->nrows == 0) return MPSG_OK;
   if (!A->cplx) {
     switch (A->K) {
-      case 2: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st, conj);
-      case 3: return launch_spmv_k<3, false>(ctx, A, order, xre, xim, yre, yim, st, conj);
-      case 4: return launch_spmv_k<4, false>(ctx, A, order, xre, xim, yre, yim, st, conj);
+      case 2: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st, conj, -2);
+      case 3: return launch_spmv_k<3, false>(ctx, A, order, xre, xim, yre, yim, st, conj, -2);
+      case 4: return launch_spmv_k<4, false>(ctx, A, order, xre, xim, yre, yim, st, conj, -2);
     }
   } else {
     switch (A->K) {
-      case 2: return launch_spmv_k<2, true>(ctx, A, order, xre, xim, yre, yim, st, conj);
-      case 3: return launch_spmv_k<3, true>(ctx, A, order, xre, xim, yre, yim, st, conj);
-      case 4: return launch_spmv_k<4, true>(ctx, A, order, xre, xim, yre, yim, st, conj);
+      case 2: return launch_spmv_k<2, true>(ctx, A, order, xre, xim, yre, yim, st, conj, -2);
+      case 3: return launch_spmv_k<3, true>(ctx, A, order, xre, xim, yre, yim, st, conj, -2);
+      case 4: return launch_spmv_k<4, true>(ctx, A, order, xre, xim, yre, yim, st, conj, -2);
     }
   }
   return fail(ctx, MPSG_E_ARG, "spmv: unsupported K %d", A->K);
 }
 
+int launch_spmv_part(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
+                     double* yre, double* yim, cudaStream_t st, bool conj, int part) {
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "spmv: unknown order %d", order);
+  if (A->nrows == 0) return MPSG_OK;
+  switch (A->K * 2 + (A->cplx ? 1 : 0)) {
+    case 4: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
+    case 5: return launch_spmv_k<2, true>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
+    case 6: return launch_spmv_k<3, false>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
+    case 7: return launch_spmv_k<3, true>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
+    case 8: return launch_spmv_k<4, false>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
+    case 9: return launch_spmv_k<4, true>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
+  }
+  return fail(ctx, MPSG_E_ARG, "spmv: unsupported K %d", A->K);
+}
+
 }  // namespace mpsg
+
+namespace {
+// Host-pointer SpMV with the result copy overlapped: x goes up, then the
+// long rows and the SELL parts (A->part_slice) run in order on the compute
+// stream, each part's rows (A->part_row) going back to the host on the copy
+// stream as soon as that part finishes.  ny = 1 (real) or 2 (complex)
+// device/host result pairs.
+int spmv_host_overlapped(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* dx0, const double* dx1,
+                         double* dy0, double* dy1, double* hy0, double* hy1, bool conj) {
+  cudaStream_t st = ctx->stream;
+  const size_t row_b = (size_t)A->K * sizeof(double);
+  const int P = (int)A->part_slice.size() - 1;
+  int rc;
+  if ((rc = launch_spmv_part(ctx, A, order, dx0, dx1, dy0, dy1, st, conj, -1))) return rc;
+  for (int p = 0; p < P; ++p) {
+    if ((rc = launch_spmv_part(ctx, A, order, dx0, dx1, dy0, dy1, st, conj, p))) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_part[p], st));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev_part[p], 0));
+    const int64_t r0 = A->part_row[(size_t)p], r1 = A->part_row[(size_t)p + 1];
+    if (r1 > r0) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(hy0 + r0 * A->K, dy0 + r0 * A->K, (size_t)(r1 - r0) * row_b,
+                                    cudaMemcpyDeviceToHost, ctx->copy));
+      if (hy1)
+        CUDA_TRY(ctx, cudaMemcpyAsync(hy1 + r0 * A->K, dy1 + r0 * A->K, (size_t)(r1 - r0) * row_b,
+                                      cudaMemcpyDeviceToHost, ctx->copy));
+    }
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->copy));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MPSG_OK;
+}
+bool can_overlap(const mpsg_ctx* ctx, const mpsg_csr* A) {
+  return ctx->overlap && ctx->copy && A->part_slice.size() >= 3 && A->part_slice.size() <= 9;
+}
+}  // namespace
 
 // ==========================================================================
 extern "C" {
@@ -145,6 +195,9 @@ int mpsg_ctx_create(int device, mpsg_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+  for (auto& ev : ctx->ev_part)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete ctx;
     return MPSG_E_CUDA;
@@ -166,6 +219,7 @@ int mpsg_ctx_create(int device, mpsg_ctx** out) {
   if (const char* s = std::getenv("MPSG_SIGMA")) ctx->sigma = std::atoll(s);
   if (const char* s = std::getenv("MPSG_FAST_CHUNK")) ctx->fast_chunk = std::atoll(s);
   if (const char* s = std::getenv("MPSG_COLBLOCK_BYTES")) ctx->colblock_bytes = std::atoll(s);
+  if (const char* s = std::getenv("MPSG_OVERLAP")) ctx->overlap = s[0] != '0';
   if (const char* s = std::getenv("MPSG_COLBLOCK_MIN")) ctx->colblock_min = std::atoll(s);
   *out = ctx;
   return MPSG_OK;
@@ -179,6 +233,9 @@ void mpsg_ctx_destroy(mpsg_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  for (auto& ev : ctx->ev_part)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -261,6 +318,21 @@ int mpsg_csr_upload_ex(mpsg_ctx* ctx, int K, int flags, int64_t nrows, int64_t n
       long_rows.push_back((int)i);
     else
       short_rows.push_back((int)i);
+  }
+  // Output parts for the host-pointer calls: consecutive sort windows write a
+  // contiguous range of y rows (plus long rows, computed first), so the
+  // device->host copy of part p overlaps the SELL launch of part p+1.
+  {
+    const int64_t W = std::max<int64_t>(1, ctx->sigma);
+    const int64_t nwin = ((int64_t)short_rows.size() + W - 1) / W;
+    const int64_t P = std::min<int64_t>(8, nwin);
+    if (P >= 2 && W % C == 0) {
+      for (int64_t p = 0; p <= P; ++p) {
+        const int64_t w = nwin * p / P;
+        A->part_slice.push_back(std::min<int64_t>(w * (W / C), ((int64_t)short_rows.size() + C - 1) / C));
+        A->part_row.push_back(p == 0 ? 0 : (p == P ? nrows : short_rows[(size_t)(w * W)]));
+      }
+    }
   }
   // stable counting sort by length, descending, inside windows of sigma rows
   {
@@ -501,6 +573,8 @@ int mpsg_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen, const d
   if ((rc = ensure_scratch(ctx, 1, yb))) return rc;
   cudaStream_t st = ctx->stream;
   if (xb) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], x, xb, cudaMemcpyHostToDevice, st));
+  if (can_overlap(ctx, A))
+    return spmv_host_overlapped(ctx, A, order, ctx->dbuf[0], nullptr, ctx->dbuf[1], nullptr, y, nullptr, false);
   if ((rc = launch_spmv(ctx, A, order, ctx->dbuf[0], nullptr, ctx->dbuf[1], nullptr, st))) return rc;
   if (yb) CUDA_TRY(ctx, cudaMemcpyAsync(y, ctx->dbuf[1], yb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
@@ -529,6 +603,9 @@ int mpsg_spmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen,
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], x_re, xb, cudaMemcpyHostToDevice, st));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[1], x_im, xb, cudaMemcpyHostToDevice, st));
   }
+  if (can_overlap(ctx, A))
+    return spmv_host_overlapped(ctx, A, order, ctx->dbuf[0], ctx->dbuf[1], ctx->dbuf[2], ctx->dbuf[3], y_re, y_im,
+                                false);
   if ((rc = launch_spmv(ctx, A, order, ctx->dbuf[0], ctx->dbuf[1], ctx->dbuf[2], ctx->dbuf[3], st))) return rc;
   if (yb) {
     CUDA_TRY(ctx, cudaMemcpyAsync(y_re, ctx->dbuf[2], yb, cudaMemcpyDeviceToHost, st));

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/mpsg.h"
 #include "layout.h"
@@ -19,6 +20,9 @@ struct mpsg_ctx {
   cudaStream_t stream = nullptr;  // current (own or caller's)
   cudaStream_t aux = nullptr;     // long-row kernels run here, forked/joined by events
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t copy = nullptr;    // device->host copies overlapped with SpMV parts
+  cudaEvent_t ev_part[8] = {};
+  bool overlap = true;            // MPSG_OVERLAP=0 disables
   std::string err;
   // scratch for host-pointer calls
   double* dbuf[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -66,9 +70,17 @@ struct mpsg_csr {
   double* partial = nullptr;
   unsigned* counter = nullptr;
   int64_t device_bytes = 0;
+  // host-call output parts: slices [part_slice[p], part_slice[p+1]) write rows
+  // [part_row[p], part_row[p+1]) (besides long rows); empty = no overlap
+  std::vector<int64_t> part_slice, part_row;
 
   SellView sell() const {
     return SellView{(int)nslices, C, slice_ptr, slot_row, slot_len, scol, sval, sell_elems};
+  }
+  // the slices [s0, s1) as a view (slice_ptr values are absolute offsets)
+  SellView sell_range(int64_t s0, int64_t s1) const {
+    return SellView{(int)(s1 - s0), C, slice_ptr + s0, slot_row + s0 * C, slot_len + s0 * C, scol, sval,
+                    sell_elems};
   }
   LongView lng() const {
     return LongView{(int)nlong, lrow, lptr, lcol, lval, long_nnz, (int)chunk, (int)nchunks,
@@ -125,11 +137,15 @@ cudaError_t launch_win(const mpsg_ctx* ctx, void (*kern)(KArgs...), dim3 grid, d
 // SpMV launch for one (K, complex) instantiation (spmv_k{2,3,4}.cu).
 template <int K, bool CPLX>
 int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre,
-                  const double* xim, double* yre, double* yim, cudaStream_t st, bool conj);
+                  const double* xim, double* yre, double* yim, cudaStream_t st, bool conj, int part = -2);
 // Dispatch over K / complex (capi.cu).  conj: complex combine of the adjoint
 // (y.re = rr + ii, y.im = ri - ir).
 int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
                 double* yre, double* yim, cudaStream_t st, bool conj = false);
+// Pieces of one SpMV: part < 0 launches the long-row kernel only (on `st`);
+// part >= 0 the SELL slices of output part `part` (A->part_slice).
+int launch_spmv_part(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
+                     double* yre, double* yim, cudaStream_t st, bool conj, int part);
 // Device CG driver for one K (cg_k{2,3,4}.cu).
 template <int K>
 int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, const double* x0,

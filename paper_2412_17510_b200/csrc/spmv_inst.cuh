@@ -7,38 +7,45 @@ namespace mpsg {
 
 // Launch every kernel of one SpMV over the device layout of A (layout.h):
 // the long-row kernel on the context's aux stream (forked/joined by events)
-// concurrently with the SELL kernel on `st`.
+// concurrently with the SELL kernel on `st`.  part = -2: all of it;
+// part = -1: only the long-row kernel, on `st`; part >= 0: only the SELL
+// slices of output part `part` (host-call overlap, capi.cu).
 template <int K, bool CPLX, bool MX, bool CONJ>
 int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
-                     double* yre, double* yim, cudaStream_t st) {
-  const bool has_long = A->nlong > 0;
+                     double* yre, double* yim, cudaStream_t st, int part) {
+  const bool has_long = A->nlong > 0 && part < 0;
+  const bool fork = has_long && part == -2;
+  cudaStream_t lst = fork ? ctx->aux : st;
   // x (re, then im for complex: one window over the first, the hotter, is
   // all a launch can carry) -- see launch_win; off unless MPSG_L2_PERSIST=1
   const size_t xb = (size_t)A->ncols * K * sizeof(double);
   if (has_long) {
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    if (fork) {
+      CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    }
     LongView L = A->lng();
     if (order == ORDER_FAST) {
       const int blocks = (int)((A->nchunks + 3) / 4);
-      CUDA_TRY(ctx, launch_win(ctx, long_fast_kernel<K, CPLX, MX, CONJ>, blocks, 128, 0, ctx->aux, xre, xb, L, xre,
-                               xim, yre, yim));
+      CUDA_TRY(ctx, launch_win(ctx, long_fast_kernel<K, CPLX, MX, CONJ>, blocks, 128, 0, lst, xre, xb, L, xre, xim,
+                               yre, yim));
     } else {
       constexpr int CH = CPLX ? 256 : 512;
       const size_t smem = (size_t)CH * (CPLX ? 4 : 1) * sizeof(MC<K>);
       if (order == ORDER_SCALAR)
         long_det_kernel<K, ORDER_SCALAR, CPLX, CH, MX, CONJ>
-            <<<(int)A->nlong, 128, smem, ctx->aux>>>(L, xre, xim, yre, yim);
+            <<<(int)A->nlong, 128, smem, lst>>>(L, xre, xim, yre, yim);
       else
         long_det_kernel<K, ORDER_LANE4, CPLX, CH, MX, CONJ>
-            <<<(int)A->nlong, 128, smem, ctx->aux>>>(L, xre, xim, yre, yim);
+            <<<(int)A->nlong, 128, smem, lst>>>(L, xre, xim, yre, yim);
     }
     CUDA_TRY(ctx, cudaGetLastError());
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));
+    if (fork) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));
   }
-  if (A->nslices > 0) {
-    const int blocks = (int)((A->nslices + 3) / 4);
-    SellView S = A->sell();
+  const SellView S = part >= 0 ? A->sell_range(A->part_slice[(size_t)part], A->part_slice[(size_t)part + 1])
+                               : A->sell();
+  if (part != -1 && S.nslices > 0) {
+    const int blocks = (S.nslices + 3) / 4;
     // Short rows: ORDER_FAST runs them in the reference's lanes-off order
     // (bit-exact with lanes off, so trivially inside the fast-mode bound) --
     // the faster of the two exact orders on B200 for every K
@@ -63,22 +70,22 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
     }
     CUDA_TRY(ctx, cudaGetLastError());
   }
-  if (has_long) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_join, 0));
+  if (fork) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_join, 0));
   return MPSG_OK;
 }
 
 template <int K, bool CPLX>
 int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
-                  double* yre, double* yim, cudaStream_t st, bool conj) {
+                  double* yre, double* yim, cudaStream_t st, bool conj, int part) {
   if constexpr (CPLX) {
     if (A->mixed)
-      return conj ? launch_spmv_mode<K, true, true, true>(ctx, A, order, xre, xim, yre, yim, st)
-                  : launch_spmv_mode<K, true, true, false>(ctx, A, order, xre, xim, yre, yim, st);
-    return conj ? launch_spmv_mode<K, true, false, true>(ctx, A, order, xre, xim, yre, yim, st)
-                : launch_spmv_mode<K, true, false, false>(ctx, A, order, xre, xim, yre, yim, st);
+      return conj ? launch_spmv_mode<K, true, true, true>(ctx, A, order, xre, xim, yre, yim, st, part)
+                  : launch_spmv_mode<K, true, true, false>(ctx, A, order, xre, xim, yre, yim, st, part);
+    return conj ? launch_spmv_mode<K, true, false, true>(ctx, A, order, xre, xim, yre, yim, st, part)
+                : launch_spmv_mode<K, true, false, false>(ctx, A, order, xre, xim, yre, yim, st, part);
   } else {
-    if (A->mixed) return launch_spmv_mode<K, false, true, false>(ctx, A, order, xre, xim, yre, yim, st);
-    return launch_spmv_mode<K, false, false, false>(ctx, A, order, xre, xim, yre, yim, st);
+    if (A->mixed) return launch_spmv_mode<K, false, true, false>(ctx, A, order, xre, xim, yre, yim, st, part);
+    return launch_spmv_mode<K, false, false, false>(ctx, A, order, xre, xim, yre, yim, st, part);
   }
 }
 
@@ -86,6 +93,6 @@ int launch_spmv_k(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre
 
 #define MPSG_INSTANTIATE_SPMV(K)                                                                            \
   template int mpsg::launch_spmv_k<K, false>(mpsg_ctx*, const mpsg_csr*, int, const double*, const double*, \
-                                             double*, double*, cudaStream_t, bool);                          \
+                                             double*, double*, cudaStream_t, bool, int);                     \
   template int mpsg::launch_spmv_k<K, true>(mpsg_ctx*, const mpsg_csr*, int, const double*, const double*,  \
-                                            double*, double*, cudaStream_t, bool);
+                                            double*, double*, cudaStream_t, bool, int);
