@@ -208,6 +208,12 @@ typedef struct mpsg_dcsr mpsg_dcsr;
 MPSG_API int mpsg_comm_unique_id(unsigned char* id);
 /* id may be NULL when nranks == 1.  NCCL is loaded at run time (libnccl.so.2). */
 MPSG_API int mpsg_comm_create(mpsg_ctx* ctx, int nranks, int rank, const unsigned char* id, mpsg_comm** out);
+/* Single-process group of nranks ranks, one mpsg_ctx each (same or different
+ * devices): collectives are device/peer copies ordered by CUDA events across
+ * the ranks' streams, no NCCL.  Every rank must be driven by its own host
+ * thread (the collectives rendezvous through a host barrier).  out[r] gets
+ * rank r's handle. */
+MPSG_API int mpsg_comm_create_local(mpsg_ctx* const* ctxs, int nranks, mpsg_comm** out);
 MPSG_API void mpsg_comm_destroy(mpsg_comm* comm);
 /* This rank's rows [row_begin, row_end) of a square nglobal x nglobal matrix:
  * indptr rebased (row_end-row_begin+1 entries), global column indices, K or

@@ -81,7 +81,7 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_comm_unique_id", "mpsg_comm_create", "mpsg_comm_destroy", "mpsg_dcsr_upload",
            "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
            "mpsg_dcg", "mpsg_halo_plan", "mpsg_csr_upload_ex", "mpsg_sptmv", "mpsg_sptmv_dev",
-           "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev")
+           "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local")
 
 CSR_COMPLEX, CSR_MIXED, CSR_TRANSPOSE = 1, 2, 4
 
@@ -123,6 +123,7 @@ def lib():
     L.mpsg_comm_unique_id.argtypes = [_P]
     L.mpsg_comm_create.argtypes = [_P, _i32, _i32, _P, ctypes.POINTER(_P)]
     L.mpsg_comm_destroy.argtypes = [_P]
+    L.mpsg_comm_create_local.argtypes = [ctypes.POINTER(_P), _i32, ctypes.POINTER(_P)]
     L.mpsg_dcsr_upload.argtypes = [_P, _i32, _i32, _i64, _i64, _i64, _P, _P, ctypes.POINTER(_P),
                                    ctypes.POINTER(_P)]
     L.mpsg_dcsr_destroy.argtypes = [_P]
@@ -466,6 +467,23 @@ class Comm:
         h = _P()
         ctx.check(lib().mpsg_comm_create(ctx.h, nranks, rank, buf, ctypes.byref(h)))
         self.h = h
+
+    @classmethod
+    def local_group(cls, ctxs):
+        """One process, one host thread per rank: comms for len(ctxs) ranks
+        whose collectives are event-ordered device/peer copies (no NCCL)."""
+        n = len(ctxs)
+        arr = (_P * n)(*[c.h for c in ctxs])
+        outs = (_P * n)()
+        rc = lib().mpsg_comm_create_local(arr, n, outs)
+        if rc != E_OK:
+            raise MpsgError(rc, "mpsg_comm_create_local failed")
+        comms = []
+        for r in range(n):
+            c = cls.__new__(cls)
+            c.ctx, c.nranks, c.rank, c.h = ctxs[r], n, r, _P(outs[r])
+            comms.append(c)
+        return comms
 
     @staticmethod
     def unique_id() -> bytes:

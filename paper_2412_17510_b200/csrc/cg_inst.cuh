@@ -165,7 +165,9 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
     long long remaining = max_iters - done_k;
     int nb = (int)std::min<long long>(batch, remaining);
     if (nb <= 0) break;
-    if (cfg->use_graph) {
+    // (a single-process group orders ranks with cross-stream events, which a
+    // stream capture cannot record: no graphs there)
+    if (cfg->use_graph && !(D && D->comm->local)) {
       if (nb != gbatch) {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);

@@ -21,7 +21,15 @@
 namespace mpsg {
 
 constexpr int CG_RUNNING = -1;
-constexpr int DOT_THREADS = 256;
+#ifndef MPSG_DOT_THREADS
+#define MPSG_DOT_THREADS 256
+#endif
+#ifdef MPSG_DOT_MINB
+#define MPSG_DOT_LB __launch_bounds__(DOT_THREADS, MPSG_DOT_MINB)
+#else
+#define MPSG_DOT_LB __launch_bounds__(DOT_THREADS)
+#endif
+constexpr int DOT_THREADS = MPSG_DOT_THREADS;
 constexpr int DOT_MAX_BLOCKS = 1024;
 
 // Device-side solver state (one per solve).
@@ -164,7 +172,7 @@ MPSG_DI void reduce_finish(CgState<K>* st, int post, MC<K> acc, double* partial,
 // contiguous segment that its threads stride through (coalesced).
 // local_out != nullptr (multi-GPU): see reduce_finish.
 template <int K, int MODE>
-__global__ void __launch_bounds__(DOT_THREADS) cg_reduce_kernel(CgState<K>* st, int post, int64_t n,
+__global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n,
                                                                 const double* u, const double* v,
                                                                 double* x, double* r, double* partial,
                                                                 int gate, double* local_out) {

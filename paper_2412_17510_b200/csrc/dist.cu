@@ -51,10 +51,62 @@ const NcclApi* NcclApi::get(std::string* err) {
   return ok ? &api : nullptr;
 }
 
+void LocalGroup::barrier() {
+  std::unique_lock<std::mutex> lk(m);
+  const long gen = generation;
+  if (++arrived == P) {
+    arrived = 0;
+    ++generation;
+    cv.notify_all();
+  } else {
+    cv.wait(lk, [&] { return generation != gen; });
+  }
+}
+
+namespace {
+// One local-group "collective": every rank publishes (ptr, ready event);
+// `pull(q, src)` enqueues this rank's copies out of rank q's buffer; then
+// every rank waits until all copies out of its own buffer are done before it
+// may overwrite it.
+template <class Pull>
+int local_collective(const mpsg_comm* c, const void* mine, cudaStream_t st, Pull pull) {
+  LocalGroup* g = c->local;
+  const int r = c->rank;
+  CUDA_TRY(c->ctx, cudaSetDevice(c->ctx->device));
+  g->ptr[(size_t)r] = mine;
+  CUDA_TRY(c->ctx, cudaEventRecord(g->ready[(size_t)r], st));
+  g->barrier();
+  for (int q = 0; q < g->P; ++q) {
+    if (q == r) continue;
+    CUDA_TRY(c->ctx, cudaStreamWaitEvent(st, g->ready[(size_t)q], 0));
+    int rc = pull(q, g->ptr[(size_t)q]);
+    if (rc) return rc;
+  }
+  CUDA_TRY(c->ctx, cudaEventRecord(g->consumed[(size_t)r], st));
+  g->barrier();
+  for (int q = 0; q < g->P; ++q)
+    if (q != r) CUDA_TRY(c->ctx, cudaStreamWaitEvent(st, g->consumed[(size_t)q], 0));
+  g->barrier();  // the events may be re-recorded by the next collective only now
+  return MPSG_OK;
+}
+}  // namespace
+
 int halo_exchange(const mpsg_dcsr* A, double* xfull, cudaStream_t st) {
   const mpsg_comm* c = A->comm;
-  if (c->nranks == 1 || A->halo_rows == 0) return MPSG_OK;
+  if (c->nranks == 1) return MPSG_OK;
   const int K = A->K;
+  if (c->local) {
+    // every rank takes part (the plan is per pair; a rank with nothing to
+    // receive still publishes its buffer for the others)
+    return local_collective(c, xfull, st, [&](int q, const void* src) -> int {
+      const int64_t rlo = A->recv[2 * q], rhi = A->recv[2 * q + 1];
+      if (rhi > rlo)
+        CUDA_TRY(c->ctx, cudaMemcpyAsync(xfull + rlo * K, static_cast<const double*>(src) + rlo * K,
+                                         (size_t)(rhi - rlo) * K * sizeof(double), cudaMemcpyDefault, st));
+      return MPSG_OK;
+    });
+  }
+  // every rank enters the group (a rank that receives nothing may still send)
   NCCL_TRY(c, c->api->GroupStart());
   for (int q = 0; q < c->nranks; ++q) {
     if (q == c->rank) continue;
@@ -70,11 +122,44 @@ int halo_exchange(const mpsg_dcsr* A, double* xfull, cudaStream_t st) {
 }
 
 int allgather_mc(const mpsg_comm* c, const double* in, double* out, int K, cudaStream_t st) {
-  if (c->nranks == 1) {
-    CUDA_TRY(c->ctx, cudaMemcpyAsync(out, in, (size_t)K * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    return MPSG_OK;
+  if (c->nranks == 1 || c->local) {
+    CUDA_TRY(c->ctx, cudaMemcpyAsync(out + (size_t)c->rank * K, in, (size_t)K * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, st));
+    if (c->nranks == 1) return MPSG_OK;
+    return local_collective(c, in, st, [&](int q, const void* src) -> int {
+      CUDA_TRY(c->ctx, cudaMemcpyAsync(out + (size_t)q * K, src, (size_t)K * sizeof(double), cudaMemcpyDefault, st));
+      return MPSG_OK;
+    });
   }
   NCCL_TRY(c, c->api->AllGather(in, out, (size_t)K, ncclDouble, c->comm, st));
+  return MPSG_OK;
+}
+
+int allgather_host(const mpsg_comm* c, const int64_t* mine, int64_t* all, int n) {
+  const int P = c->nranks;
+  if (P == 1) {
+    std::copy(mine, mine + n, all);
+    return MPSG_OK;
+  }
+  if (c->local) {
+    LocalGroup* g = c->local;
+    std::copy(mine, mine + n, g->meta.begin() + (size_t)c->rank * n);
+    g->barrier();
+    std::copy(g->meta.begin(), g->meta.begin() + (size_t)P * n, all);
+    g->barrier();
+    return MPSG_OK;
+  }
+  mpsg_ctx* ctx = c->ctx;
+  int64_t* d = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&d, sizeof(int64_t) * n * (P + 1)));
+  cudaStream_t st = ctx->stream;
+  cudaMemcpyAsync(d, mine, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st);
+  ncclResult_t r = c->api->AllGather(d, d + n, (size_t)n, ncclInt64, c->comm, st);
+  cudaMemcpyAsync(all, d + n, sizeof(int64_t) * n * P, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (r != ncclSuccess) return fail(ctx, MPSG_E_NCCL, "setup allgather: %s", c->api->GetErrorString(r));
+  if (e != cudaSuccess) return fail(ctx, MPSG_E_CUDA, "setup allgather: %s", cudaGetErrorString(e));
   return MPSG_OK;
 }
 
@@ -161,9 +246,58 @@ int mpsg_comm_create(mpsg_ctx* ctx, int nranks, int rank, const unsigned char* i
   return MPSG_OK;
 }
 
+int mpsg_comm_create_local(mpsg_ctx* const* ctxs, int nranks, mpsg_comm** out) {
+  if (!ctxs || !out || nranks < 1) return MPSG_E_ARG;
+  auto* g = new LocalGroup();
+  g->P = nranks;
+  g->ptr.assign((size_t)nranks, nullptr);
+  g->ready.assign((size_t)nranks, nullptr);
+  g->consumed.assign((size_t)nranks, nullptr);
+  g->meta.assign((size_t)nranks * 8, 0);
+  for (int r = 0; r < nranks; ++r) {
+    out[r] = nullptr;
+    if (!ctxs[r]) return MPSG_E_ARG;
+  }
+  for (int r = 0; r < nranks; ++r) {
+    mpsg_ctx* ctx = ctxs[r];
+    cudaSetDevice(ctx->device);
+    if (cudaEventCreateWithFlags(&g->ready[(size_t)r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->consumed[(size_t)r], cudaEventDisableTiming) != cudaSuccess)
+      return fail(ctx, MPSG_E_CUDA, "comm_create_local: event creation failed");
+    for (int q = 0; q < nranks; ++q)  // peer access between distinct devices (best effort)
+      if (ctxs[q]->device != ctx->device) {
+        cudaDeviceEnablePeerAccess(ctxs[q]->device, 0);
+        cudaGetLastError();
+      }
+    auto* c = new mpsg_comm();
+    c->ctx = ctx;
+    c->nranks = nranks;
+    c->rank = r;
+    c->local = g;
+    out[r] = c;
+  }
+  g->refs = nranks;
+  return MPSG_OK;
+}
+
 void mpsg_comm_destroy(mpsg_comm* c) {
   if (!c) return;
   if (c->comm && c->api) c->api->CommDestroy(c->comm);
+  if (c->local) {
+    mpsg::LocalGroup* g = c->local;
+    bool last;
+    {
+      std::lock_guard<std::mutex> lk(g->m);
+      last = --g->refs == 0;
+    }
+    if (last) {
+      for (auto e : g->ready)
+        if (e) cudaEventDestroy(e);
+      for (auto e : g->consumed)
+        if (e) cudaEventDestroy(e);
+      delete g;
+    }
+  }
   delete c;
 }
 
@@ -196,20 +330,7 @@ int mpsg_dcsr_upload(mpsg_comm* c, int K, int is_complex, int64_t nglobal, int64
   // every rank's row block and read interval (tiny allgather at setup)
   const int P = c->nranks;
   std::vector<int64_t> mine = {row_begin, row_end, lo, hi}, all((size_t)4 * P);
-  if (P == 1) {
-    all = mine;
-  } else {
-    int64_t* d = nullptr;
-    CUDA_TRY(ctx, cudaMalloc(&d, sizeof(int64_t) * 4 * (P + 1)));
-    cudaStream_t st = ctx->stream;
-    cudaMemcpyAsync(d, mine.data(), sizeof(int64_t) * 4, cudaMemcpyHostToDevice, st);
-    ncclResult_t r = c->api->AllGather(d, d + 4, 4, ncclInt64, c->comm, st);
-    cudaMemcpyAsync(all.data(), d + 4, sizeof(int64_t) * 4 * P, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(d);
-    if (r != ncclSuccess) return fail(ctx, MPSG_E_NCCL, "dcsr_upload allgather: %s", c->api->GetErrorString(r));
-    if (e != cudaSuccess) return fail(ctx, MPSG_E_CUDA, "dcsr_upload: %s", cudaGetErrorString(e));
-  }
+  if ((rc = allgather_host(c, mine.data(), all.data(), 4))) return rc;
   A->bounds.assign((size_t)P + 1, 0);
   A->need.assign((size_t)2 * P, 0);
   for (int q = 0; q < P; ++q) {

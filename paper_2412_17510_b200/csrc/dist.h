@@ -19,6 +19,8 @@
 #pragma once
 #include <nccl.h>
 
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -41,6 +43,27 @@ struct NcclApi {
   static const NcclApi* get(std::string* err);
 };
 
+// Single-process group: one host thread per rank (each with its own
+// mpsg_ctx, on one or several devices), data moved by device-to-device /
+// peer copies ordered with CUDA events across the ranks' streams, and a host
+// barrier to publish each collective's buffers and events.  No kernel ever
+// waits on another rank's kernel (only stream-order dependencies), so ranks
+// may share a GPU.  Used for single-process multi-GPU runs and to exercise the
+// sharded path on one GPU.
+struct LocalGroup {
+  int P = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long generation = 0;
+  std::vector<const void*> ptr;       // per rank: buffer published for the collective
+  std::vector<cudaEvent_t> ready;     // per rank: its buffer is complete
+  std::vector<cudaEvent_t> consumed;  // per rank: its copies out of the others are done
+  std::vector<int64_t> meta;          // per rank: 4 int64 (setup allgather)
+  int refs = 0;
+  void barrier();
+};
+
 }  // namespace mpsg
 
 struct mpsg_comm {
@@ -48,6 +71,7 @@ struct mpsg_comm {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   const mpsg::NcclApi* api = nullptr;
+  mpsg::LocalGroup* local = nullptr;  // single-process group backend (instead of NCCL)
 };
 
 struct mpsg_dcsr {
@@ -78,6 +102,8 @@ namespace mpsg {
 int halo_exchange(const mpsg_dcsr* A, double* xfull, cudaStream_t st);
 // out[P*K] = every rank's in[K] (rank order).
 int allgather_mc(const mpsg_comm* c, const double* in, double* out, int K, cudaStream_t st);
+// Host allgather of n int64 per rank (setup only).
+int allgather_host(const mpsg_comm* c, const int64_t* mine, int64_t* all, int n);
 
 // Distributed device CG (cg_inst.cuh), b / x0 / x_out are this rank's block.
 template <int K>

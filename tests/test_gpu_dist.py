@@ -86,3 +86,108 @@ def test_one_rank_dcg_with_initial_guess_and_graph_off(ctx):
     assert r1.report.converged and r2.report.converged
     assert abs(r1.report.iterations - r2.report.iterations) <= 1
     assert np.allclose(r1.x[:, 0], xt[:, 0], atol=1e-12)
+
+
+# ---- several ranks on one GPU: the single-process group backend ------------------
+def _run_ranks(P, fn):
+    """fn(rank, comm, ctx) on P host threads, one context and comm per rank."""
+    import threading
+
+    ctxs = [M.Context(0) for _ in range(P)]
+    comms = M.Comm.local_group(ctxs)
+    out, errs = [None] * P, []
+
+    def body(r):
+        try:
+            out[r] = fn(r, comms[r], ctxs[r])
+        except Exception as e:  # noqa: BLE001
+            errs.append((r, repr(e)))
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not errs, errs
+    for c in comms:
+        c.close()
+    for c in ctxs:
+        c.close()
+    return out
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("cfg,K,p1,p2,p3", [(4, 2, 20000, 5000.0, 1.8), (5, 4, 24, 0.0, 0.0), (2, 3, 5000, 32.0, 0.0)])
+def test_sharded_spmv_several_ranks_bit_exact(P, cfg, K, p1, p2, p3):
+    A = synth.config_matrix(cfg, K, p1, p2, p3)
+    x = synth.config_vector(cfg, A.nrows, K)
+    bounds = M.partition_rows(A.indptr, A.nrows, P)
+
+    def rank_fn(r, comm, ctx):
+        dA = M.DistCsr.from_global(comm, A, K, bounds=bounds)
+        b, e = dA.row_begin, dA.row_end
+        res = {o: M.dspmv(dA, x[b:e], o) for o in (0, 1, 2)}
+        dA.close()
+        return res
+
+    parts = _run_ranks(P, rank_fn)
+    for o in (0, 1):
+        y = np.concatenate([p[o] for p in parts])
+        assert bits_equal(y, O.spmv(A, x, o)), (P, o)
+    # FAST: same kernels per shard, long rows reordered -> equal to the single-GPU FAST result
+    yf = np.concatenate([p[2] for p in parts])
+    assert bits_equal(yf, M.spmv(M.DeviceCsr(A, K), x, 2))
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_complex_several_ranks(P):
+    import torch
+
+    K = 2
+    A = synth.config_matrix(3, K, 3000, 16.0)
+    xr, xi = synth.config_vector(3, A.nrows, K)
+    bounds = M.partition_rows(A.indptr, A.nrows, P)
+
+    def rank_fn(r, comm, ctx):
+        dA = M.DistCsr.from_global(comm, A, K, is_complex=True, bounds=bounds)
+        b, e = dA.row_begin, dA.row_end
+        with torch.cuda.device(0):
+            dxr, dxi = torch.from_numpy(xr[b:e].copy()).cuda(), torch.from_numpy(xi[b:e].copy()).cuda()
+            dyr, dyi = torch.empty_like(dxr), torch.empty_like(dxi)
+        M.dspmv_complex_dev(dA, dxr.data_ptr(), dxi.data_ptr(), dyr.data_ptr(), dyi.data_ptr(), 1)
+        ctx.synchronize()
+        out = dyr.cpu().numpy(), dyi.cpu().numpy()
+        dA.close()
+        return out
+
+    parts = _run_ranks(P, rank_fn)
+    rr, ri = O.spmv_complex(A, xr, xi, 1)
+    assert bits_equal(np.concatenate([p[0] for p in parts]), rr)
+    assert bits_equal(np.concatenate([p[1] for p in parts]), ri)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("K", [2, 4])
+def test_sharded_cg_several_ranks(P, K):
+    A = synth.config_matrix(5, K, 16)
+    xt = synth.config_vector(5, A.nrows, K)
+    b = O.spmv(A, xt, 1)
+    bounds = M.partition_rows(A.indptr, A.nrows, P)
+    cfg = M.SolverConfig(rel_tol=1e-22, max_iters=300)
+
+    def rank_fn(r, comm, ctx):
+        dA = M.DistCsr.from_global(comm, A, K, bounds=bounds)
+        res = M.dsolve_cg(dA, b[dA.row_begin:dA.row_end], cfg)
+        dA.close()
+        return res
+
+    parts = _run_ranks(P, rank_fn)
+    single = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, K)), b, cfg)
+    h0 = parts[0].report.residual_history
+    for p in parts[1:]:  # every rank took the same decisions on the same numbers
+        assert p.report.residual_history == h0 and p.report.iterations == parts[0].report.iterations
+    assert parts[0].report.status == single.report.status
+    assert abs(parts[0].report.iterations - single.report.iterations) <= 1
+    x = np.concatenate([p.x for p in parts])
+    assert np.allclose(x[:, 0], xt[:, 0], atol=1e-12)
+    assert parts[0].report.final_true_residual <= 10 * single.report.final_true_residual + 1e-30
