@@ -249,6 +249,11 @@ MPSG_API uint64_t mpsg_checksum(int K, int64_t n, const double* v);
 MPSG_API uint64_t mpsg_checksum_complex(int K, int64_t n, const double* re, const double* im);
 MPSG_API const char* mpsg_version(void);
 
+/* The reference harness's input vectors (make_vector / make_complex_vector,
+ * bench.hpp:78-111), computed with the device ops (the reference's bits):
+ * im == NULL: re[j] = sqrt(2) * (j+1); else re + i im = sqrt(2 + 3i) * (j+1). */
+MPSG_API int mpsg_make_vector(mpsg_ctx* ctx, int K, int64_t n, double* re, double* im);
+
 /* ---- measurement / verification -------------------------------------- */
 /* fp64-pipe throughput (DFMA instructions per second) on the context device:
  * the roofline denominator for the fp64-bound TD/QD configurations. */

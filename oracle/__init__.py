@@ -235,6 +235,8 @@ def ref():
         L.ref_spmv_complex.restype = _i32
         L.ref_sptmv_complex.argtypes = [_P, _P, _i32, _i32, _i32, _P]
         L.ref_sptmv_complex.restype = _i32
+        L.ref_mtx_spmv.argtypes = [ctypes.c_char_p, _i32, _i32, _i32, _i32, _i32, _P, _P, _P]
+        L.ref_mtx_spmv.restype = _i32
         L.ref_mc_op.argtypes = [_i32, _i32, _P, _P, _P]
         L.ref_make_vector.argtypes = [_i32, _i64, _P]
         L.ref_make_complex_vector.argtypes = [_i32, _i64, _P, _P]
@@ -396,6 +398,18 @@ def ref_sptmv_complex(A, vr, vi, order=LANE4, threads=1, conjugate=False, mixed=
     if ref().ref_sptmv_complex(Ah.h, xh.h, order, threads, 1 if conjugate else 0, yh.h) != 0:
         raise ValueError(ref().ref_last_error().decode())
     return yh.read(A.ncols)
+
+
+def ref_mtx_spmv(path, K, mixed=False, lanes=True, threads=1, transposed=False):
+    """The reference CLI's spmv pipeline on a Matrix Market file (parse_mtx ->
+    coo_to_csr / split_complex -> make_vector -> spmv / sptmv -> checksum):
+    returns (checksum, n, nnz)."""
+    h, n, nz = np.zeros(1, np.uint64), np.zeros(1, np.int64), np.zeros(1, np.int64)
+    rc = ref().ref_mtx_spmv(str(path).encode(), K, 1 if mixed else 0, 1 if lanes else 0, threads,
+                            1 if transposed else 0, _p(h), _p(n), _p(nz))
+    if rc != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return int(h[0]), int(n[0]), int(nz[0])
 
 
 def ref_cg(A, b, order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters=10000):

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "mps/bench.hpp"
+#include "mps/mtxio.hpp"
 #include "mps/kernels.hpp"
 #include "mps/krylov.hpp"
 #include "support/fixtures.hpp"
@@ -426,6 +427,33 @@ int ref_csr_export(void* hh, int64_t* indptr, int64_t* indices, double* vals) {
   std::memcpy(indices, m.indices.data(), m.indices.size() * sizeof(int64_t));
   for (int64_t k = 0; k < m.nnz(); ++k) vals[k] = m.values.get(static_cast<size_t>(k));
   return 0;
+}
+
+// The reference CLI's spmv pipeline (tools/mpsparse.cpp:74-97 -> time_kernel,
+// src/bench.cpp:192-253) on a Matrix Market file: returns the record's
+// checksum and fills n / nnz.  K = 2, 3, 4; mixed = binary64 matrix.
+int ref_mtx_spmv(const char* path, int K, int mixed, int lanes, int threads, int transposed, uint64_t* checksum_out,
+                 int64_t* n_out, int64_t* nnz_out) {
+  return guard([&] {
+    auto parsed = parse_mtx_file(path, true);
+    KernelRequest req;
+    req.precision = K == 2 ? PrecisionTag::dd() : K == 3 ? PrecisionTag::td() : PrecisionTag::qd();
+    req.matrix_mode = mixed ? MatrixMode::MixedBinary64 : MatrixMode::Pure;
+    req.threads = threads;
+    req.lanes_enabled = lanes != 0;
+    req.repetitions = 1;
+    BenchRecord rec;
+    if (is_complex(parsed)) {
+      req.kernel = transposed ? KernelKind::SptmvComplex : KernelKind::SpmvComplex;
+      rec = time_kernel(split_complex(std::get<CooMatrix<std::complex<double>>>(parsed)), "m", req);
+    } else {
+      req.kernel = transposed ? KernelKind::Sptmv : KernelKind::Spmv;
+      rec = time_kernel(coo_to_csr(std::get<CooMatrix<double>>(parsed)), "m", req);
+    }
+    *checksum_out = rec.checksum;
+    *n_out = rec.n;
+    *nnz_out = rec.nnz;
+  });
 }
 
 }  // extern "C"

@@ -54,9 +54,53 @@ __global__ void mc_op_kernel(int op, int64_t n, const double* a, const double* b
   store_aos<K>(out, i, r);
 }
 
+// The reference harness's input vectors (bench.hpp:78-111), evaluated with
+// the device restatement of the reference ops, so the bits are the
+// reference's: v_j = sqrt(2) * j; complex v_j = sqrt(2 + 3i) * j with
+// Re = sqrt((sqrt(13) + 2) / 2), Im = sqrt((sqrt(13) - 2) / 2).
+template <int K>
+__global__ void make_vector_kernel(int64_t n, double* re, double* im) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const MC<K> j = from_double<K>((double)(i + 1));
+  if (!im) {
+    store_aos<K>(re, i, mul(sqrt_mc(from_double<K>(2.0)), j));
+    return;
+  }
+  const MC<K> half = from_double<K>(0.5), two = from_double<K>(2.0);
+  const MC<K> root13 = sqrt_mc(from_double<K>(13.0));
+  const MC<K> r = sqrt_mc(mul(add(root13, two), half));
+  const MC<K> m = sqrt_mc(mul(sub(root13, two), half));
+  store_aos<K>(re, i, mul(r, j));
+  store_aos<K>(im, i, mul(m, j));
+}
+
 }  // namespace
 
 extern "C" {
+
+MPSG_API int mpsg_make_vector(mpsg_ctx* ctx, int K, int64_t n, double* re, double* im) {
+  if (!ctx || !re || n < 1) return MPSG_E_ARG;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t b = (size_t)n * K * sizeof(double);
+  double *d = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&d, b * (im ? 2 : 1)));
+  cudaStream_t st = ctx->stream;
+  const unsigned blocks = (unsigned)((n + 127) / 128);
+  double* dim = im ? d + (size_t)n * K : nullptr;
+  switch (K) {
+    case 2: make_vector_kernel<2><<<blocks, 128, 0, st>>>(n, d, dim); break;
+    case 3: make_vector_kernel<3><<<blocks, 128, 0, st>>>(n, d, dim); break;
+    case 4: make_vector_kernel<4><<<blocks, 128, 0, st>>>(n, d, dim); break;
+    default: cudaFree(d); return fail(ctx, MPSG_E_ARG, "make_vector: K must be 2, 3 or 4");
+  }
+  cudaError_t e = cudaMemcpyAsync(re, d, b, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && im) e = cudaMemcpyAsync(im, dim, b, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(ctx, MPSG_E_CUDA, "make_vector: %s", cudaGetErrorString(e));
+  return MPSG_OK;
+}
 
 MPSG_API int mpsg_measure_fp64_peak(mpsg_ctx* ctx, double* ops_per_s) {
   if (!ctx || !ops_per_s) return MPSG_E_ARG;
