@@ -81,7 +81,7 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_comm_unique_id", "mpsg_comm_create", "mpsg_comm_destroy", "mpsg_dcsr_upload",
            "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
            "mpsg_dcg", "mpsg_halo_plan", "mpsg_csr_upload_ex", "mpsg_sptmv", "mpsg_sptmv_dev",
-           "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local")
+           "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local", "mpsg_make_vector")
 
 CSR_COMPLEX, CSR_MIXED, CSR_TRANSPOSE = 1, 2, 4
 
@@ -124,6 +124,7 @@ def lib():
     L.mpsg_comm_create.argtypes = [_P, _i32, _i32, _P, ctypes.POINTER(_P)]
     L.mpsg_comm_destroy.argtypes = [_P]
     L.mpsg_comm_create_local.argtypes = [ctypes.POINTER(_P), _i32, ctypes.POINTER(_P)]
+    L.mpsg_make_vector.argtypes = [_P, _i32, _i64, _P, _P]
     L.mpsg_dcsr_upload.argtypes = [_P, _i32, _i32, _i64, _i64, _i64, _P, _P, ctypes.POINTER(_P),
                                    ctypes.POINTER(_P)]
     L.mpsg_dcsr_destroy.argtypes = [_P]
@@ -662,6 +663,15 @@ MC_OPS = {"add": 0, "mul": 1, "mul_d": 2, "sub": 3, "div": 4, "sqrt": 5}
 def mc_op_dev(ctx: Context, op: str, K: int, n: int, d_a: int, d_b: int, d_out: int):
     """Batched device MC op on AoS device arrays (asynchronous on the context stream)."""
     ctx.check(lib().mpsg_mc_op_dev(ctx.h, MC_OPS[op], K, n, d_a, d_b, d_out))
+
+
+def make_vector(ctx: Context, K: int, n: int, complex: bool = False):
+    """The reference harness's input vector (bench.hpp:78-111): v_j = sqrt(2) j,
+    or (re, im) of sqrt(2 + 3i) j, computed on the device with the reference's ops."""
+    re = np.empty((n, K))
+    im = np.empty((n, K)) if complex else None
+    ctx.check(lib().mpsg_make_vector(ctx.h, K, n, _p(re), _p(im)))
+    return (re, im) if complex else re
 
 
 def version() -> str:
