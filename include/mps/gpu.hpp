@@ -31,8 +31,9 @@
 //  * KernelMode::lanes_enabled selects the accumulation order, reproduced bit
 //    for bit (true: row_sum_lanes_*, kernels.hpp:103-142; false:
 //    row_sum_scalar, kernels.hpp:90).  KernelMode::threads has no device
-//    meaning for spmv and is ignored; sptmv reproduces the reference at one
-//    thread (lanes do not change its bits).  The overloads taking
+//    meaning for spmv and is ignored; sptmv reproduces the reference at that
+//    thread count (its per-thread accumulators are merged in thread order;
+//    lanes do not change its bits).  The overloads taking
 //    mps::gpu::Order::Fast select the throughput order (componentwise error
 //    bound instead of bits).
 //  * dimension errors throw std::invalid_argument with the reference message
@@ -47,6 +48,7 @@
 #pragma once
 
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -191,17 +193,19 @@ std::vector<F> spmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, const Ker
   return spmv(A, v, order_of(mode));
 }
 
+// threads: the reference sptmv's OpenMP thread count, whose per-thread
+// accumulators are merged in thread order (kernels.hpp:368-394) -- reproduced
 template <class E, class F>
-std::vector<F> sptmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, Order order) {
+std::vector<F> sptmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, Order order, int threads = 1) {
   std::vector<F> y(static_cast<std::size_t>(A.cols()));
-  A.context().check(mpsg_sptmv(A.context().get(), A.get(), static_cast<int>(order),
-                               static_cast<std::int64_t>(v.size()), reinterpret_cast<const double*>(v.data()),
-                               reinterpret_cast<double*>(y.data())));
+  A.context().check(mpsg_sptmv_ex(A.context().get(), A.get(), static_cast<int>(order), threads,
+                                  static_cast<std::int64_t>(v.size()), reinterpret_cast<const double*>(v.data()),
+                                  reinterpret_cast<double*>(y.data())));
   return y;
 }
 template <class E, class F>
 std::vector<F> sptmv(const DeviceCsr<E, F>& A, const std::vector<F>& v, const KernelMode& mode) {
-  return sptmv(A, v, order_of(mode));
+  return sptmv(A, v, order_of(mode), std::max(1, mode.threads));
 }
 
 template <class E, class F>
@@ -225,13 +229,13 @@ ComplexVector<F> spmv_complex(const DeviceCsr<E, F>& A, const ComplexVector<F>& 
 
 template <class E, class F>
 ComplexVector<F> sptmv_complex(const DeviceCsr<E, F>& A, const ComplexVector<F>& v, Order order,
-                               bool conjugate = false) {
+                               bool conjugate = false, int threads = 1) {
   if (v.re.size() != v.im.size()) throw std::invalid_argument("sptmv_complex: re/im vector length mismatch");
   ComplexVector<F> y;
   y.re.resize(static_cast<std::size_t>(A.cols()));
   y.im.resize(static_cast<std::size_t>(A.cols()));
-  A.context().check(mpsg_sptmv_complex(A.context().get(), A.get(), static_cast<int>(order), conjugate ? 1 : 0,
-                                       static_cast<std::int64_t>(v.re.size()),
+  A.context().check(mpsg_sptmv_complex_ex(A.context().get(), A.get(), static_cast<int>(order), threads,
+                                          conjugate ? 1 : 0, static_cast<std::int64_t>(v.re.size()),
                                        reinterpret_cast<const double*>(v.re.data()),
                                        reinterpret_cast<const double*>(v.im.data()),
                                        reinterpret_cast<double*>(y.re.data()),
@@ -333,7 +337,7 @@ ComplexVector<F> sptmv_complex(const ComplexSparseMatrix<E>& A, const ComplexVec
   if (v.re.size() != v.im.size()) throw std::invalid_argument("sptmv_complex: re/im vector length mismatch");
   if (static_cast<std::size_t>(A.re.nrows) != v.re.size())
     throw std::invalid_argument(detail::dim_msg("sptmv", v.re.size(), A.re.nrows));
-  return sptmv_complex(detail::cached<E, F>(A, true), v, order_of(mode), conjugate);
+  return sptmv_complex(detail::cached<E, F>(A, true), v, order_of(mode), conjugate, std::max(1, mode.threads));
 }
 
 // nnz-balanced contiguous row bounds (kernels.hpp:63-80)
@@ -367,7 +371,7 @@ struct GpuCsrOperator {
   }
   template <class F>
   std::vector<F> apply_transposed(const std::vector<F>& x) const {
-    return gpu::sptmv(*matrix, x, order());
+    return gpu::sptmv(*matrix, x, order(), threads);  // the reference's thread-count-dependent merge
   }
 };
 

@@ -181,9 +181,18 @@ MPSG_API int mpsg_spmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, 
 MPSG_API int mpsg_sptmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t vlen, const double* v, double* y);
 MPSG_API int mpsg_sptmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_v, double* d_y,
                             void* stream);
+/* The reference sptmv at `threads` OpenMP threads: per-thread accumulators
+ * over partition_rows(threads) row blocks merged in thread order
+ * (kernels.hpp:368-394) -- thread-count dependent bits, reproduced exactly in
+ * the exact orders (threads <= 1: as mpsg_sptmv). */
+MPSG_API int mpsg_sptmv_ex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads, int64_t vlen,
+                           const double* v, double* y);
 /* conjugate != 0: the adjoint A^H v (y.re = rr + ii, y.im = ri - ir). */
 MPSG_API int mpsg_sptmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugate, int64_t vlen,
                                 const double* v_re, const double* v_im, double* y_re, double* y_im);
+MPSG_API int mpsg_sptmv_complex_ex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads, int conjugate,
+                                   int64_t vlen, const double* v_re, const double* v_im, double* y_re,
+                                   double* y_im);
 MPSG_API int mpsg_sptmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugate,
                                     const double* d_v_re, const double* d_v_im, double* d_y_re, double* d_y_im,
                                     void* stream);

@@ -81,7 +81,8 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_comm_unique_id", "mpsg_comm_create", "mpsg_comm_destroy", "mpsg_dcsr_upload",
            "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
            "mpsg_dcg", "mpsg_halo_plan", "mpsg_csr_upload_ex", "mpsg_sptmv", "mpsg_sptmv_dev",
-           "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local", "mpsg_make_vector")
+           "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local", "mpsg_make_vector",
+           "mpsg_sptmv_ex", "mpsg_sptmv_complex_ex")
 
 CSR_COMPLEX, CSR_MIXED, CSR_TRANSPOSE = 1, 2, 4
 
@@ -125,6 +126,8 @@ def lib():
     L.mpsg_comm_destroy.argtypes = [_P]
     L.mpsg_comm_create_local.argtypes = [ctypes.POINTER(_P), _i32, ctypes.POINTER(_P)]
     L.mpsg_make_vector.argtypes = [_P, _i32, _i64, _P, _P]
+    L.mpsg_sptmv_ex.argtypes = [_P, _P, _i32, _i32, _i64, _P, _P]
+    L.mpsg_sptmv_complex_ex.argtypes = [_P, _P, _i32, _i32, _i32, _i64, _P, _P, _P, _P]
     L.mpsg_dcsr_upload.argtypes = [_P, _i32, _i32, _i64, _i64, _i64, _P, _P, ctypes.POINTER(_P),
                                    ctypes.POINTER(_P)]
     L.mpsg_dcsr_destroy.argtypes = [_P]
@@ -301,14 +304,20 @@ def spmv_complex(A: DeviceCsr, v_re, v_im, mode: KernelMode | int | None = None)
     return yr, yi
 
 
+def _threads(mode) -> int:
+    return max(1, int(getattr(mode, "threads", 1) or 1))
+
+
 def sptmv(A: DeviceCsr, v, mode: KernelMode | int | None = None) -> np.ndarray:
-    """y = A^T v (kernels.hpp:368-394); the exact orders equal the reference
-    sptmv at one thread.  Needs ``DeviceCsr(..., transpose=True)``."""
+    """y = A^T v (kernels.hpp:368-394).  The exact orders equal the reference
+    sptmv at ``mode.threads`` OpenMP threads (its per-thread accumulators are
+    merged in thread order, so the bits depend on the thread count).  Needs
+    ``DeviceCsr(..., transpose=True)``."""
     x = _aos(v, "sptmv")
     if x.shape[1] != A.K:
         raise ValueError(f"sptmv: vector has K={x.shape[1]} components, matrix has K={A.K}")
     y = np.empty((A.ncols, A.K))
-    A.ctx.check(lib().mpsg_sptmv(A.ctx.h, A.h, _order(mode), x.shape[0], _p(x), _p(y)))
+    A.ctx.check(lib().mpsg_sptmv_ex(A.ctx.h, A.h, _order(mode), _threads(mode), x.shape[0], _p(x), _p(y)))
     return y
 
 
@@ -318,8 +327,8 @@ def sptmv_complex(A: DeviceCsr, v_re, v_im, mode: KernelMode | int | None = None
     if xr.shape[0] != xi.shape[0]:
         raise ValueError("sptmv_complex: re/im vector length mismatch")
     yr, yi = np.empty((A.ncols, A.K)), np.empty((A.ncols, A.K))
-    A.ctx.check(lib().mpsg_sptmv_complex(A.ctx.h, A.h, _order(mode), 1 if conjugate else 0, xr.shape[0], _p(xr),
-                                         _p(xi), _p(yr), _p(yi)))
+    A.ctx.check(lib().mpsg_sptmv_complex_ex(A.ctx.h, A.h, _order(mode), _threads(mode), 1 if conjugate else 0,
+                                            xr.shape[0], _p(xr), _p(xi), _p(yr), _p(yi)))
     return yr, yi
 
 

@@ -230,6 +230,7 @@ void mpsg_ctx_destroy(mpsg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (auto& p : ctx->dbuf)
     if (p) cudaFree(p);
+  if (ctx->seg_bounds) cudaFree(ctx->seg_bounds);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
@@ -508,6 +509,7 @@ int mpsg_csr_upload_ex(mpsg_ctx* ctx, int K, int flags, int64_t nrows, int64_t n
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (bad) return fail(ctx, MPSG_E_RANGE, "csr_upload: column index outside [0, %lld)", (long long)ncols);
   if (flags & MPSG_CSR_TRANSPOSE) {
+    A->host_indptr.assign(indptr, indptr + nrows + 1);
     // A^T on the host (stable counting sort by column, as transpose_csr,
     // sparse.hpp:139-163: the rows of A^T list their entries in ascending
     // original row), uploaded as its own device matrix.  Row j of A^T summed
@@ -640,7 +642,38 @@ int mpsg_sptmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_
   return launch_spmv(ctx, T, torder(order), d_v, nullptr, d_y, nullptr, st);
 }
 
+namespace {
+// Segment bounds of the reference's T-thread sptmv (partition_rows of A) for
+// the launch that follows; cleared again by SegScope's destructor.
+struct SegScope {
+  mpsg_ctx* ctx;
+  ~SegScope() { ctx->seg_T = 1; }
+};
+int set_segments(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads) {
+  ctx->seg_T = 1;
+  if (threads <= 1 || order == MPSG_ORDER_FAST || A->nrows == 0) return MPSG_OK;
+  ctx->seg_host.assign((size_t)threads + 1, 0);
+  mpsg_partition_rows(A->host_indptr.data(), A->nrows, threads, ctx->seg_host.data());
+  const size_t b = ctx->seg_host.size() * sizeof(int64_t);
+  if (ctx->seg_cap < b) {
+    if (ctx->seg_bounds) cudaFree(ctx->seg_bounds);
+    ctx->seg_bounds = nullptr;
+    ctx->seg_cap = 0;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->seg_bounds, b));
+    ctx->seg_cap = b;
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->seg_bounds, ctx->seg_host.data(), b, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->seg_T = threads;
+  return MPSG_OK;
+}
+}  // namespace
+
 int mpsg_sptmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t vlen, const double* v, double* y) {
+  return mpsg_sptmv_ex(ctx, A, order, 1, vlen, v, y);
+}
+
+int mpsg_sptmv_ex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads, int64_t vlen, const double* v,
+                  double* y) {
   if (!ctx || !A) return MPSG_E_ARG;
   if (vlen != A->nrows) return fail(ctx, MPSG_E_DIM, "%s", dim_msg("sptmv", vlen, A->nrows).c_str());
   if (A->cplx) return fail(ctx, MPSG_E_ARG, "sptmv: matrix is complex, use mpsg_sptmv_complex");
@@ -654,6 +687,8 @@ int mpsg_sptmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t vlen, const 
   cudaStream_t st = ctx->stream;
   if (vb) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], v, vb, cudaMemcpyHostToDevice, st));
   if (yb && T->nnz == 0) CUDA_TRY(ctx, cudaMemsetAsync(ctx->dbuf[1], 0, yb, st));
+  SegScope scope{ctx};
+  if ((rc = set_segments(ctx, A, order, threads))) return rc;
   if ((rc = launch_spmv(ctx, T, torder(order), ctx->dbuf[0], nullptr, ctx->dbuf[1], nullptr, st))) return rc;
   if (yb) CUDA_TRY(ctx, cudaMemcpyAsync(y, ctx->dbuf[1], yb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
@@ -674,6 +709,11 @@ int mpsg_sptmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conj
 
 int mpsg_sptmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugate, int64_t vlen,
                        const double* v_re, const double* v_im, double* y_re, double* y_im) {
+  return mpsg_sptmv_complex_ex(ctx, A, order, 1, conjugate, vlen, v_re, v_im, y_re, y_im);
+}
+
+int mpsg_sptmv_complex_ex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads, int conjugate, int64_t vlen,
+                          const double* v_re, const double* v_im, double* y_re, double* y_im) {
   if (!ctx || !A) return MPSG_E_ARG;
   if (!A->cplx) return fail(ctx, MPSG_E_ARG, "sptmv_complex: matrix is real");
   if (vlen != A->nrows) return fail(ctx, MPSG_E_DIM, "%s", dim_msg("sptmv", vlen, A->nrows).c_str());
@@ -693,6 +733,8 @@ int mpsg_sptmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int conjugat
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->dbuf[2], 0, yb, st));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->dbuf[3], 0, yb, st));
   }
+  SegScope scope{ctx};
+  if ((rc = set_segments(ctx, A, order, threads))) return rc;
   if ((rc = launch_spmv(ctx, T, torder(order), ctx->dbuf[0], ctx->dbuf[1], ctx->dbuf[2], ctx->dbuf[3], st,
                         conjugate != 0)))
     return rc;

@@ -23,6 +23,12 @@ struct mpsg_ctx {
   cudaStream_t copy = nullptr;    // device->host copies overlapped with SpMV parts
   cudaEvent_t ev_part[8] = {};
   bool overlap = true;            // MPSG_OVERLAP=0 disables
+  // transposed product at T > 1 threads: segment bounds of the running call
+  // (set by mpsg_sptmv*_ex around the launch; seg_T == 1 means off)
+  int64_t* seg_bounds = nullptr;
+  size_t seg_cap = 0;
+  int seg_T = 1;
+  std::vector<int64_t> seg_host;
   std::string err;
   // scratch for host-pointer calls
   double* dbuf[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -47,6 +53,7 @@ struct mpsg_csr {
   bool cplx = false;
   bool mixed = false;         // binary64 values (Mixed mode, kernels.hpp:55-58)
   mpsg_csr* trans = nullptr;  // device transpose, for the transposed products
+  std::vector<int64_t> host_indptr;  // A's row pointer (kept with the transpose: thread partition)
   int64_t nrows = 0, ncols = 0, nnz = 0;
   // SELL store
   int C = 32;

@@ -32,7 +32,10 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
     } else {
       constexpr int CH = CPLX ? 256 : 512;
       const size_t smem = (size_t)CH * (CPLX ? 4 : 1) * sizeof(MC<K>);
-      if (order == ORDER_SCALAR)
+      if (order == ORDER_SCALAR && ctx->seg_T > 1)
+        long_det_kernel<K, ORDER_SCALAR, CPLX, CH, MX, CONJ, true>
+            <<<(int)A->nlong, 128, smem, lst>>>(L, xre, xim, yre, yim, ctx->seg_bounds, ctx->seg_T);
+      else if (order == ORDER_SCALAR)
         long_det_kernel<K, ORDER_SCALAR, CPLX, CH, MX, CONJ>
             <<<(int)A->nlong, 128, smem, lst>>>(L, xre, xim, yre, yim);
       else
@@ -51,8 +54,11 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
     // the faster of the two exact orders on B200 for every K
     // (profiles/r01b_variants.txt); only long rows are reordered.
     const int sorder = order == ORDER_FAST ? ORDER_SCALAR : order;
+    const bool seg = order == ORDER_SCALAR && ctx->seg_T > 1;
     if constexpr (!CPLX) {
-      if (sorder == ORDER_SCALAR)
+      if (seg)
+        sell_real_seg_kernel<K, MX><<<blocks, 128, 0, st>>>(S, xre, yre, ctx->seg_bounds, ctx->seg_T);
+      else if (sorder == ORDER_SCALAR)
         CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_SCALAR, MX>, blocks, 128, 0, st, xre, xb, S, xre,
                                  yre));
       else if constexpr (K == 2)
@@ -61,12 +67,15 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
         CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_LANE4, MX>, blocks, 128, 0, st, xre, xb, S, xre,
                                  yre));
     } else {
-      if (sorder == ORDER_SCALAR)
+      if (seg)
+        sell_complex_kernel<K, ORDER_SCALAR, MX, CONJ, true>
+            <<<blocks, 128, 0, st>>>(S, xre, xim, yre, yim, ctx->seg_bounds, ctx->seg_T);
+      else if (sorder == ORDER_SCALAR)
         CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_SCALAR, MX, CONJ>, blocks, 128, 0, st, xre, xb,
-                                 S, xre, xim, yre, yim));
+                                 S, xre, xim, yre, yim, nullptr, 1));
       else
         CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_LANE4, MX, CONJ>, blocks, 128, 0, st, xre, xb,
-                                 S, xre, xim, yre, yim));
+                                 S, xre, xim, yre, yim, nullptr, 1));
     }
     CUDA_TRY(ctx, cudaGetLastError());
   }

@@ -176,6 +176,39 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
   return acc;
 }
 
+// Transposed product at T threads (kernels.hpp:368-394): the reference gives
+// each of T row blocks (partition_rows) its own zero accumulator and merges
+// them in thread order, y = acc_0, then y = y + acc_t for t = 1..T-1 -- for
+// every output, touched or not.  On A^T (row j = column j of A, entries in
+// ascending original row i) that is a fold over the T segments of row j cut at
+// bounds[t]: each segment summed from zero in row order, the segment sums
+// added in order.  `SegFold` walks one row's entries and does exactly that.
+template <int K>
+struct SegFold {
+  const int64_t* bounds;
+  int T, t;
+  int64_t next;
+  MC<K> y, acc;
+  MPSG_DI SegFold(const int64_t* b, int T_) : bounds(b), T(T_), t(0), next(__ldg(b + 1)), y(zero<K>()), acc(zero<K>()) {}
+  MPSG_DI void close() {
+    if (t == 0)
+      y = acc;
+    else
+      y = add(y, acc);
+    acc = zero<K>();
+    ++t;
+    next = t < T ? __ldg(bounds + t + 1) : INT64_MAX;
+  }
+  MPSG_DI void push(int64_t i, const MC<K>& p) {  // entry of original row i
+    while (i >= next) close();
+    acc = add(acc, p);
+  }
+  MPSG_DI MC<K> finish() {
+    while (t < T) close();
+    return y;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // SELL slice, real: one warp per slice of 32 rows, one thread per row.
 // ---------------------------------------------------------------------------
@@ -216,6 +249,29 @@ __global__ void __launch_bounds__(128, 12) sell_real_lane4_lat_kernel(SellView S
   sell_real_body<K, ORDER_LANE4, MX>(S, x, y);
 }
 
+// Transposed product at T > 1 threads, real (see SegFold).
+template <int K, bool MX>
+__global__ void __launch_bounds__(128) sell_real_seg_kernel(SellView S, const double* __restrict__ x,
+                                                            double* __restrict__ y, const int64_t* segb, int segT) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= S.nslices) return;
+  const int slot = s * 32 + lane;
+  const int row = S.slot_row[slot];
+  const int len = S.slot_len[slot];
+  const int64_t base = S.slice_ptr[s] + lane;
+  SegFold<K> f(segb, segT);
+  for (int k = 0; k < len; ++k) {
+    const int64_t e = base + (int64_t)k * 32;
+    const int c = ld_s32_stream(S.col + e);
+    AVal<K, MX> a;
+    a.load(S.val, S.stride, e);
+    f.push(c, a.times(load_aos<K>(x, c)));
+  }
+  const MC<K> r = f.finish();
+  if (row >= 0) store_aos<K>(y, row, r);
+}
+
 // ---------------------------------------------------------------------------
 // SELL slice, complex: one warp per slice of 16 rows, two threads per row.
 // Lanes 0-15 ("re" half) own rr = A.re x.re and ri = A.re x.im; lanes 16-31
@@ -234,11 +290,12 @@ MPSG_DI void complex_store(double* __restrict__ yre, double* __restrict__ yim, i
   }
 }
 
-template <int K, int ORDER, bool MX, bool CONJ>
+template <int K, int ORDER, bool MX, bool CONJ, bool SEG = false>
 __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const double* __restrict__ xre,
                                                            const double* __restrict__ xim,
                                                            double* __restrict__ yre,
-                                                           double* __restrict__ yim) {
+                                                           double* __restrict__ yim,
+                                                           const int64_t* segb = nullptr, int segT = 1) {
   const int lane = threadIdx.x & 31;
   const int t = lane & 15;
   const bool imh = lane >= 16;
@@ -256,7 +313,19 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
   const double* __restrict__ x2 = imh ? xre : xim;
 
   MC<K> s1 = zero<K>(), s2 = zero<K>();
-  if constexpr (ORDER == ORDER_SCALAR) {
+  if constexpr (SEG) {  // transposed product at T > 1 threads (SegFold), per sum
+    SegFold<K> f1(segb, segT), f2(segb, segT);
+    for (int k = 0; k < len; ++k) {
+      const int64_t e = (int64_t)k * 16;
+      const int c = ld_s32_stream(cp + e);
+      AVal<K, MX> a;
+      a.load(vp, st, e);
+      f1.push(c, a.times(load_aos<K>(x1, c)));
+      f2.push(c, a.times(load_aos<K>(x2, c)));
+    }
+    s1 = f1.finish();
+    s2 = f2.finish();
+  } else if constexpr (ORDER == ORDER_SCALAR) {
     int c = len > 0 ? ld_s32_stream(cp) : 0;  // column index loaded a round ahead
     for (int k = 0; k < len; ++k) {
       const int64_t e = (int64_t)k * 16;
@@ -326,11 +395,12 @@ MPSG_DI void long_products(const LongView& L, int64_t k, const double* __restric
   }
 }
 
-template <int K, int ORDER, bool CPLX, int CH, bool MX, bool CONJ>
+template <int K, int ORDER, bool CPLX, int CH, bool MX, bool CONJ, bool SEG = false>
 __global__ void __launch_bounds__(128) long_det_kernel(LongView L, const double* __restrict__ xre,
                                                        const double* __restrict__ xim,
                                                        double* __restrict__ yre,
-                                                       double* __restrict__ yim) {
+                                                       double* __restrict__ yim,
+                                                       const int64_t* segb = nullptr, int segT = 1) {
   constexpr int NS = CPLX ? 4 : 1;
   constexpr int NL = (ORDER == ORDER_LANE4) ? 4 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -345,13 +415,16 @@ __global__ void __launch_bounds__(128) long_det_kernel(LongView L, const double*
   const bool chain = tid < NS * NL;
   const int sidx = tid / NL, lj = tid % NL;
   MC<K> acc = zero<K>();
+  SegFold<K> fold(SEG ? segb : L.ptr, SEG ? segT : 1);  // SEG: transposed product at T > 1 threads
   int64_t c0 = 0;
   for (; c0 < len; c0 += CH) {
     const int cnt = (int)((len - c0) < CH ? (len - c0) : CH);
     for (int i = tid; i < cnt; i += blockDim.x) long_products<K, CPLX, MX>(L, b + c0 + i, xre, xim, prod + i * NS);
     __syncthreads();
     if (chain) {
-      if constexpr (ORDER == ORDER_LANE4) {
+      if constexpr (SEG) {
+        for (int i = 0; i < cnt; ++i) fold.push(L.col[b + c0 + i], prod[i * NS + sidx]);
+      } else if constexpr (ORDER == ORDER_LANE4) {
         for (int i = lj; i < cnt && c0 + i < m4; i += 4) acc = add(acc, prod[i * NS + sidx]);
       } else {
         for (int i = 0; i < cnt; ++i) acc = add(acc, prod[i * NS + sidx]);
@@ -360,6 +433,9 @@ __global__ void __launch_bounds__(128) long_det_kernel(LongView L, const double*
     if (c0 + CH < len) __syncthreads();
   }
   c0 -= CH;  // start of the last chunk (still resident in shared memory)
+  if constexpr (SEG) {
+    if (chain) acc = fold.finish();
+  }
   // all chain threads live in warp 0
   if (tid < 32) {
     MC<K> s = acc;

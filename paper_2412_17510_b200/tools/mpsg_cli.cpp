@@ -20,8 +20,9 @@
 //   run_spmv / run_solve tools/mpsparse.cpp:74-134
 // The matrix is uploaded once (outside the timing, as the reference converts
 // before timing, bench.cpp:211-213); each timed call is the host-pointer SpMV.
-// --threads is recorded (the device has no thread count); sptmv reproduces the
-// reference at one thread.  --lanes fast selects the throughput order.
+// --threads is recorded; it changes nothing for spmv (rows are independent)
+// and selects the reference's thread-order merge for sptmv (kernels.hpp:368-394),
+// reproduced bit for bit.  --lanes fast selects the throughput order.
 #include <algorithm>
 #include <chrono>
 #include <cinttypes>
@@ -280,11 +281,13 @@ int run_spmv(const Args& a) {
   check(ctx, mpsg_make_vector(ctx, K, n, vr.data(), cplx ? vi.data() : nullptr), "make_vector");
   auto run = [&] {
     int rc;
+    const int thr = a.threads > 0 ? a.threads : 1;  // sptmv's bits depend on the thread count
     if (cplx)
-      rc = a.transposed ? mpsg_sptmv_complex(ctx, d, order, 0, n, vr.data(), vi.data(), yr.data(), yi.data())
-                        : mpsg_spmv_complex(ctx, d, order, n, vr.data(), vi.data(), yr.data(), yi.data());
+      rc = a.transposed
+               ? mpsg_sptmv_complex_ex(ctx, d, order, thr, 0, n, vr.data(), vi.data(), yr.data(), yi.data())
+               : mpsg_spmv_complex(ctx, d, order, n, vr.data(), vi.data(), yr.data(), yi.data());
     else
-      rc = a.transposed ? mpsg_sptmv(ctx, d, order, n, vr.data(), yr.data())
+      rc = a.transposed ? mpsg_sptmv_ex(ctx, d, order, thr, n, vr.data(), yr.data())
                         : mpsg_spmv(ctx, d, order, n, vr.data(), yr.data());
     check(ctx, rc, "spmv");
   };

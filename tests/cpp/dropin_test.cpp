@@ -220,6 +220,11 @@ void mixed_and_transposed(test::Rng& rng) {
   KernelMode one{{}, MatrixMode::Pure, false, 1, true};
   report(same_bits(mps::sptmv(A, u, one), mps::gpu::sptmv(A, u, one)),
          "pure K=" + std::to_string(K) + " sptmv (500x700) bit-exact with the reference at one thread");
+  for (int t : {3, 5}) {  // per-thread accumulators merged in thread order (kernels.hpp:368-394)
+    KernelMode mt{{}, MatrixMode::Pure, false, t, true};
+    report(same_bits(mps::sptmv(A, u, mt), mps::gpu::sptmv(A, u, mt)),
+           "pure K=" + std::to_string(K) + " sptmv bit-exact with the reference at " + std::to_string(t) + " threads");
+  }
   auto cm = convert_complex_csr<E>(split_complex(test::random_complex_coo(rng, 300, 260, 7000)));
   for (std::size_t i = 0; i < cm.re.indices.size(); ++i) {
     cm.re.values.set(i, rng.multicomp<K>(-4, 4));
@@ -231,6 +236,11 @@ void mixed_and_transposed(test::Rng& rng) {
     auto g = mps::gpu::sptmv_complex(cm, cv, one, conj);
     report(same_bits(r.re, g.re) && same_bits(r.im, g.im),
            "complex K=" + std::to_string(K) + (conj ? " adjoint" : " transpose") + " sptmv_complex bit-exact");
+    KernelMode m4{{}, MatrixMode::Pure, false, 4, false};
+    auto r4 = mps::sptmv_complex(cm, cv, m4, conj);
+    auto g4 = mps::gpu::sptmv_complex(cm, cv, m4, conj);
+    report(same_bits(r4.re, g4.re) && same_bits(r4.im, g4.im),
+           "complex K=" + std::to_string(K) + (conj ? " adjoint" : " transpose") + " sptmv_complex bit-exact at 4 threads");
   }
 }
 

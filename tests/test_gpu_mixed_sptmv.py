@@ -167,3 +167,34 @@ def test_against_reference_goldens(ctx, key):
         vr, vi = synth.config_vector(3, A.nrows, K)
         yr, yi = M.sptmv_complex(M.DeviceCsr(A, K, True, ctx=ctx, transpose=True), vr, vi, 1, conjugate=True)
         assert bits_equal(yr, g[key + "_re"]) and bits_equal(yi, g[key + "_im"])
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+@pytest.mark.parametrize("threads", [2, 3, 5, 16])
+@pytest.mark.parametrize("mixed", [False, True])
+def test_sptmv_thread_count_merge_bit_exact(K, threads, mixed):
+    """The reference sptmv at T threads: per-thread accumulators merged in thread
+    order (oracle restatement pinned to the reference for T = 1, 2, 5)."""
+    c = M.Context(0)
+    c.set_layout(long_threshold=64)
+    A = synth.config_matrix(4, K, 3000, 800.0, 1.8)
+    rows = [sorted(set(A.indices[A.indptr[i]:A.indptr[i + 1]].tolist()) | {3}) for i in range(A.nrows)]
+    from tests.util import csr
+
+    B = csr(A.nrows, A.ncols, rows, K, seed=2)  # dense column 3: a long row of B^T
+    if mixed:
+        B = mixed_of(B)
+    v = synth.vector(synth.VAL_NORMAL, B.nrows, K, seed=4)
+    dB = M.DeviceCsr(B, K, ctx=c, mixed=mixed, transpose=True)
+    for order in (0, 1):
+        y = M.sptmv(dB, v, M.KernelMode(threads=threads, lanes_enabled=order == 1))
+        ref = O.sptmv(B, v, threads=threads, mixed=mixed)
+        assert bits_equal(y, ref), first_mismatch(y, ref)
+    C = synth.config_matrix(3, K, 400, 24.0)
+    vr, vi = synth.config_vector(3, C.nrows, K)
+    dC = M.DeviceCsr(C, K, True, ctx=c, transpose=True)
+    for conj in (False, True):
+        yr, yi = M.sptmv_complex(dC, vr, vi, M.KernelMode(threads=threads), conjugate=conj)
+        rr, ri = O.sptmv_complex(C, vr, vi, threads, conj)
+        assert bits_equal(yr, rr) and bits_equal(yi, ri)
+    c.close()
