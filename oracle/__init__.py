@@ -71,6 +71,9 @@ def orc():
         L.orc_cg.argtypes = [_i32, _i32, _i64, _P, _P, _P, _P, _f64, _f64, _i64, _P, _P, _P, _P,
                              _P, _P]
         L.orc_cg.restype = _i32
+        L.orc_solve.argtypes = [_i32, _i32, _i32, _i32, _i64, _P, _P, _P, _P, _P, _f64, _f64, _i64, _P, _P,
+                                _P, _P, _P, _P, _P]
+        L.orc_solve.restype = _i32
         _orc = L
     return _orc
 
@@ -192,6 +195,43 @@ def cg(A, b, order=LANE4, rel_tol=1e-13, abs_tol=1e-99, max_iters=10000):
                 rhs_norm=float(rhs[0]), final_true_residual=float(tr[0]))
 
 
+METHODS = ("cg", "bicg", "cgs", "bicgstab", "gpbicg")  # KrylovMethod order, krylov.hpp:24
+REASONS = {1: "<p, Ap> vanished", 2: "non-finite residual", 3: "<r~, r> vanished", 4: "<p~, Ap> vanished",
+           5: "<r~, Ap> vanished", 6: "<t, t> vanished", 7: "omega vanished", 8: "<At, At> vanished",
+           9: "zeta/eta system is singular", 10: "zeta vanished"}
+
+
+def _method_id(method) -> int:
+    return METHODS.index(method) if isinstance(method, str) else int(method)
+
+
+def detail_text(method, reason: int) -> str:
+    return f"{METHODS[_method_id(method)]}: {REASONS[reason]}" if reason else ""
+
+
+def solve(A, b, method="bicgstab", order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters=10000,
+          x0=None):
+    """C restatement of solve() (krylov.hpp:596-606): every method, sequential
+    dots, CsrOperator products (sptmv at `threads`)."""
+    K = b.shape[1]
+    n = A.nrows
+    x = np.zeros((n, K))
+    hist = np.zeros(max_iters + 2)
+    iters = np.zeros(1, np.int64)
+    status, reason = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    rhs, tr = np.zeros(1), np.zeros(1)
+    x0a = None if x0 is None else np.ascontiguousarray(np.asarray(x0, np.float64))
+    nh = orc().orc_solve(_method_id(method), K, order, threads, n, _p(_c(A.indptr, np.int64)),
+                         _p(_c(A.indices, np.int64)), _p(_c(A.planes[:K])), _p(_c(b)),
+                         None if x0a is None else _p(x0a), rel_tol, abs_tol, max_iters, _p(x), _p(hist),
+                         _p(iters), _p(status), _p(reason), _p(rhs), _p(tr))
+    if nh < 0:
+        raise ValueError("solver: invalid configuration")
+    return dict(x=x, history=hist[:nh].copy(), iterations=int(iters[0]), status=int(status[0]),
+                rhs_norm=float(rhs[0]), final_true_residual=float(tr[0]),
+                final_recurrence_residual=float(hist[nh - 1]), detail=detail_text(method, int(reason[0])))
+
+
 # --------------------------------------------------------------------------- real reference
 _ref = None
 
@@ -243,6 +283,9 @@ def ref():
         L.ref_cg.argtypes = [_P, _P, _i32, _i32, _f64, _f64, _i64, _P, _P, _i64, _P, _P, _P, _P, _P,
                              ctypes.c_char_p, _i32]
         L.ref_cg.restype = _i64
+        L.ref_solve.argtypes = [_P, _P, _i32, _i32, _i32, _f64, _f64, _i64, _P, _P, _P, _i64, _P, _P, _P,
+                                _P, _P, ctypes.c_char_p, _i32]
+        L.ref_solve.restype = _i64
         L.ref_fixture.argtypes = [ctypes.c_char_p, _u64, _i64, _i64, _i64]
         L.ref_fixture.restype = _P
         L.ref_csr_info.argtypes = [_P, _P, _P, _P]
@@ -423,6 +466,28 @@ def ref_cg(A, b, order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters
     detail = ctypes.create_string_buffer(256)
     nh = ref().ref_cg(Ah.h, bh.h, order, threads, rel_tol, abs_tol, max_iters, _p(x), _p(hist),
                       len(hist), _p(iters), _p(status), _p(rhs), _p(tr), _p(fr), detail, 256)
+    if nh < 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return dict(x=x, history=hist[:nh].copy(), iterations=int(iters[0]), status=int(status[0]),
+                rhs_norm=float(rhs[0]), final_true_residual=float(tr[0]),
+                final_recurrence_residual=float(fr[0]), detail=detail.value.decode())
+
+
+def ref_solve(A, b, method="bicgstab", order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters=10000,
+              x0=None):
+    """The reference solve() itself (oracle/_ref) on the same inputs."""
+    K = b.shape[1]
+    Ah, bh = RefCsr(A, K), RefVec(b)
+    x = np.zeros((A.nrows, K))
+    hist = np.zeros(max_iters + 2)
+    iters = np.zeros(1, np.int64)
+    status = np.zeros(1, np.int32)
+    rhs, tr, fr = np.zeros(1), np.zeros(1), np.zeros(1)
+    detail = ctypes.create_string_buffer(256)
+    x0a = None if x0 is None else np.ascontiguousarray(np.asarray(x0, np.float64))
+    nh = ref().ref_solve(Ah.h, bh.h, _method_id(method), order, threads, rel_tol, abs_tol, max_iters,
+                         None if x0a is None else _p(x0a), _p(x), _p(hist), len(hist), _p(iters), _p(status),
+                         _p(rhs), _p(tr), _p(fr), detail, 256)
     if nh < 0:
         raise ValueError(ref().ref_last_error().decode())
     return dict(x=x, history=hist[:nh].copy(), iterations=int(iters[0]), status=int(status[0]),

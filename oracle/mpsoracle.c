@@ -643,3 +643,469 @@ ORC_API int orc_cg(int K, int lanes, int64_t n, const int64_t *indptr, const int
   free(q);
   return (int)nh;
 }
+
+/* ------------------------------------------------------ Krylov solvers ---
+ * krylov.hpp:238-594 -- solve_cg, solve_bicg, solve_cgs, solve_bicgstab,
+ * solve_gpbicg, dispatched on `method` like solve() :596-606 (KrylovMethod
+ * order, krylov.hpp:24).  Common parts: solver_init :160-201 (x0 :174-181),
+ * record_step :203-213, close_report :215-224, finish_true_residual
+ * :226-232, tiny :234.  The operator is CsrOperator (krylov.hpp:101-120):
+ * apply = spmv in the lanes order, apply_transposed = sptmv at `threads`.
+ * reason codes (the SolverReport detail text after "<method>: "):
+ *   1 "<p, Ap> vanished"  2 "non-finite residual"  3 "<r~, r> vanished"
+ *   4 "<p~, Ap> vanished" 5 "<r~, Ap> vanished"    6 "<t, t> vanished"
+ *   7 "omega vanished"    8 "<At, At> vanished"    9 "zeta/eta system is singular"
+ *  10 "zeta vanished" */
+typedef struct {
+  int K, lanes, threads;
+  int64_t n;
+  const int64_t *indptr, *indices;
+  const double *vals;
+  double thr[4], cap, floor;
+  double *hist;
+  int64_t nh;
+} KrCtx;
+
+static void kr_apply(const KrCtx *c, const double *x, double *y) {
+  orc_spmv(c->K, c->lanes, 0, c->n, c->n, c->n, c->indptr, c->indices, c->vals, x, y);
+}
+static void kr_apply_t(const KrCtx *c, const double *x, double *y) {
+  orc_sptmv(c->K, 0, c->threads, c->n, c->n, c->n, c->indptr, c->indices, c->vals, x, y);
+}
+static void kr_axpy(int K, int64_t n, const double *alpha, const double *x, double *y) {
+  double t[4];
+  for (int64_t i = 0; i < n; ++i) {
+    orc_mul(K, alpha, x + i * K, t);
+    orc_add(K, y + i * K, t, y + i * K);
+  }
+}
+static void kr_norm2(int K, int64_t n, const double *v, double *out) {
+  double d[4];
+  vdot(K, n, v, v, d);
+  orc_sqrt(K, d, out);
+}
+static void kr_neg(int K, const double *a, double *r) {
+  for (int j = 0; j < K; ++j) r[j] = -a[j];
+}
+static int kr_tiny(double v, double floor) { return !isfinite(v) || fabs(v) < floor; }
+static int kr_le(int K, const double *a, const double *b) {
+  int c = orc_compare(K, a, b);
+  return c == 0 || c == -1;
+}
+/* record_step: 0 continue, 1 converged, 2 diverged, 3 non-finite */
+static int kr_record(KrCtx *c, const double *rnorm) {
+  double rd = orc_to_double(c->K, rnorm);
+  c->hist[c->nh++] = rd;
+  if (!isfinite(rd)) return 3;
+  if (kr_le(c->K, rnorm, c->thr)) return 1;
+  if (rd > c->cap) return 2;
+  return 0;
+}
+/* step -> (status, reason) as close_report is called after a stop */
+static void kr_stop(int step, int *status, int *reason) {
+  *status = step == 1 ? 0 : step == 2 ? 3 : 2;
+  *reason = step == 3 ? 2 : 0;
+}
+
+#define KR_VEC(name) double *name = (double *)calloc((size_t)(n * K) + 1, sizeof(double))
+#define KR_BREAK(why, it) \
+  do {                    \
+    *status = 2;          \
+    *reason = (why);      \
+    *iters = (it);        \
+    goto out;             \
+  } while (0)
+#define KR_RECORD(rn)                     \
+  do {                                    \
+    int step_ = kr_record(c, (rn));       \
+    if (step_) {                          \
+      kr_stop(step_, status, reason);     \
+      *iters = k;                         \
+      goto out;                           \
+    }                                     \
+  } while (0)
+
+static void kr_cg(KrCtx *c, double *x, double *r, int64_t max_iters, int64_t *iters, int *status,
+                  int *reason) {
+  const int K = c->K;
+  const int64_t n = c->n;
+  KR_VEC(p);
+  KR_VEC(q);
+  double rho[4], sigma[4], alpha[4], ma[4], rn[4], rho_next[4], beta[4], t[4];
+  int64_t k;
+  memcpy(p, r, sizeof(double) * (size_t)(n * K));
+  vdot(K, n, r, r, rho);
+  for (k = 1; k <= max_iters; ++k) {
+    kr_apply(c, p, q);
+    vdot(K, n, p, q, sigma);
+    if (kr_tiny(orc_to_double(K, sigma), c->floor)) KR_BREAK(1, k - 1);
+    orc_div(K, rho, sigma, alpha);
+    kr_neg(K, alpha, ma);
+    kr_axpy(K, n, alpha, p, x);
+    kr_axpy(K, n, ma, q, r);
+    vdot(K, n, r, r, rho_next);
+    orc_sqrt(K, rho_next, rn);
+    KR_RECORD(rn);
+    orc_div(K, rho_next, rho, beta);
+    for (int64_t i = 0; i < n; ++i) {
+      orc_mul(K, beta, p + i * K, t);
+      orc_add(K, r + i * K, t, p + i * K);
+    }
+    memcpy(rho, rho_next, sizeof(rho));
+  }
+  *status = 1;
+  *iters = max_iters;
+out:
+  free(p);
+  free(q);
+}
+
+static void kr_bicg(KrCtx *c, double *x, double *r, int64_t max_iters, int64_t *iters, int *status,
+                    int *reason) {
+  const int K = c->K;
+  const int64_t n = c->n;
+  const size_t vb = sizeof(double) * (size_t)(n * K);
+  KR_VEC(rt);
+  KR_VEC(p);
+  KR_VEC(pt);
+  KR_VEC(q);
+  KR_VEC(qt);
+  double rho[4], sigma[4], alpha[4], ma[4], rn[4], rho_next[4], beta[4], t[4];
+  int64_t k;
+  memcpy(rt, r, vb);
+  memcpy(p, r, vb);
+  memcpy(pt, rt, vb);
+  vdot(K, n, rt, r, rho);
+  for (k = 1; k <= max_iters; ++k) {
+    if (kr_tiny(orc_to_double(K, rho), c->floor)) KR_BREAK(3, k - 1);
+    kr_apply(c, p, q);
+    kr_apply_t(c, pt, qt);
+    vdot(K, n, pt, q, sigma);
+    if (kr_tiny(orc_to_double(K, sigma), c->floor)) KR_BREAK(4, k - 1);
+    orc_div(K, rho, sigma, alpha);
+    kr_neg(K, alpha, ma);
+    kr_axpy(K, n, alpha, p, x);
+    kr_axpy(K, n, ma, q, r);
+    kr_axpy(K, n, ma, qt, rt);
+    kr_norm2(K, n, r, rn);
+    KR_RECORD(rn);
+    vdot(K, n, rt, r, rho_next);
+    orc_div(K, rho_next, rho, beta);
+    for (int64_t i = 0; i < n; ++i) {
+      orc_mul(K, beta, p + i * K, t);
+      orc_add(K, r + i * K, t, p + i * K);
+      orc_mul(K, beta, pt + i * K, t);
+      orc_add(K, rt + i * K, t, pt + i * K);
+    }
+    memcpy(rho, rho_next, sizeof(rho));
+  }
+  *status = 1;
+  *iters = max_iters;
+out:
+  free(rt);
+  free(p);
+  free(pt);
+  free(q);
+  free(qt);
+}
+
+static void kr_cgs(KrCtx *c, double *x, double *r, int64_t max_iters, int64_t *iters, int *status,
+                   int *reason) {
+  const int K = c->K;
+  const int64_t n = c->n;
+  const size_t vb = sizeof(double) * (size_t)(n * K);
+  KR_VEC(rt);
+  KR_VEC(u);
+  KR_VEC(p);
+  KR_VEC(q);
+  KR_VEC(v);
+  KR_VEC(tv);
+  KR_VEC(w);
+  double rho[4], sigma[4], alpha[4], ma[4], rn[4], rho_next[4], beta[4], t[4], t2[4];
+  int64_t k;
+  memcpy(rt, r, vb);
+  memcpy(u, r, vb);
+  memcpy(p, r, vb);
+  vdot(K, n, rt, r, rho);
+  for (k = 1; k <= max_iters; ++k) {
+    if (kr_tiny(orc_to_double(K, rho), c->floor)) KR_BREAK(3, k - 1);
+    kr_apply(c, p, v);
+    vdot(K, n, rt, v, sigma);
+    if (kr_tiny(orc_to_double(K, sigma), c->floor)) KR_BREAK(5, k - 1);
+    orc_div(K, rho, sigma, alpha);
+    for (int64_t i = 0; i < n; ++i) { /* q = u - alpha v; t = u + q */
+      orc_mul(K, alpha, v + i * K, t);
+      orc_sub(K, u + i * K, t, q + i * K);
+      orc_add(K, u + i * K, q + i * K, tv + i * K);
+    }
+    kr_axpy(K, n, alpha, tv, x);
+    kr_apply(c, tv, w);
+    kr_neg(K, alpha, ma);
+    kr_axpy(K, n, ma, w, r);
+    kr_norm2(K, n, r, rn);
+    KR_RECORD(rn);
+    vdot(K, n, rt, r, rho_next);
+    orc_div(K, rho_next, rho, beta);
+    for (int64_t i = 0; i < n; ++i) { /* u = r + beta q; p = u + beta (q + beta p) */
+      orc_mul(K, beta, q + i * K, t);
+      orc_add(K, r + i * K, t, u + i * K);
+      orc_mul(K, beta, p + i * K, t);
+      orc_add(K, q + i * K, t, t2);
+      orc_mul(K, beta, t2, t);
+      orc_add(K, u + i * K, t, p + i * K);
+    }
+    memcpy(rho, rho_next, sizeof(rho));
+  }
+  *status = 1;
+  *iters = max_iters;
+out:
+  free(rt);
+  free(u);
+  free(p);
+  free(q);
+  free(v);
+  free(tv);
+  free(w);
+}
+
+static void kr_bicgstab(KrCtx *c, double *x, double *r, int64_t max_iters, int64_t *iters, int *status,
+                        int *reason) {
+  const int K = c->K;
+  const int64_t n = c->n;
+  const size_t vb = sizeof(double) * (size_t)(n * K);
+  KR_VEC(rt);
+  KR_VEC(p);
+  KR_VEC(v);
+  KR_VEC(s);
+  KR_VEC(tv);
+  double rho[4], sigma[4], alpha[4], ma[4], rn[4], sn[4], tt[4], ts[4], omega[4], mo[4], rho_next[4],
+      beta[4], q1[4], q2[4], t[4], t2[4];
+  int64_t k;
+  memcpy(rt, r, vb);
+  memcpy(p, r, vb);
+  vdot(K, n, rt, r, rho);
+  for (k = 1; k <= max_iters; ++k) {
+    if (kr_tiny(orc_to_double(K, rho), c->floor)) KR_BREAK(3, k - 1);
+    kr_apply(c, p, v);
+    vdot(K, n, rt, v, sigma);
+    if (kr_tiny(orc_to_double(K, sigma), c->floor)) KR_BREAK(5, k - 1);
+    orc_div(K, rho, sigma, alpha);
+    kr_neg(K, alpha, ma);
+    memcpy(s, r, vb);
+    kr_axpy(K, n, ma, v, s);
+    kr_norm2(K, n, s, sn);
+    if (kr_le(K, sn, c->thr)) { /* half step converged (krylov.hpp:449-458) */
+      kr_axpy(K, n, alpha, p, x);
+      memcpy(r, s, vb);
+      c->hist[c->nh++] = orc_to_double(K, sn);
+      *status = 0;
+      *reason = 0;
+      *iters = k;
+      goto out;
+    }
+    kr_apply(c, s, tv);
+    vdot(K, n, tv, tv, tt);
+    if (kr_tiny(orc_to_double(K, tt), c->floor)) KR_BREAK(6, k - 1);
+    vdot(K, n, tv, s, ts);
+    orc_div(K, ts, tt, omega);
+    if (kr_tiny(orc_to_double(K, omega), c->floor)) KR_BREAK(7, k - 1);
+    kr_axpy(K, n, alpha, p, x);
+    kr_axpy(K, n, omega, s, x);
+    memcpy(r, s, vb);
+    kr_neg(K, omega, mo);
+    kr_axpy(K, n, mo, tv, r);
+    kr_norm2(K, n, r, rn);
+    KR_RECORD(rn);
+    vdot(K, n, rt, r, rho_next);
+    orc_div(K, rho_next, rho, q1);
+    orc_div(K, alpha, omega, q2);
+    orc_mul(K, q1, q2, beta);
+    for (int64_t i = 0; i < n; ++i) { /* p = r + beta (p - omega v) */
+      orc_mul(K, omega, v + i * K, t);
+      orc_sub(K, p + i * K, t, t2);
+      orc_mul(K, beta, t2, t);
+      orc_add(K, r + i * K, t, p + i * K);
+    }
+    memcpy(rho, rho_next, sizeof(rho));
+  }
+  *status = 1;
+  *iters = max_iters;
+out:
+  free(rt);
+  free(p);
+  free(v);
+  free(s);
+  free(tv);
+}
+
+static void kr_gpbicg(KrCtx *c, double *x, double *r, int64_t max_iters, int64_t *iters, int *status,
+                      int *reason) {
+  const int K = c->K;
+  const int64_t n = c->n;
+  const size_t vb = sizeof(double) * (size_t)(n * K);
+  KR_VEC(rt);
+  KR_VEC(p);
+  KR_VEC(tp);
+  KR_VEC(w);
+  KR_VEC(u);
+  KR_VEC(z);
+  KR_VEC(y);
+  KR_VEC(ap);
+  KR_VEC(tv);
+  KR_VEC(at);
+  double rho[4], sigma[4], alpha[4], ma[4], rn[4], tn[4], att[4], ata[4], yy[4], yat[4], yt[4], zeta[4],
+      eta[4], me[4], mz[4], rho_next[4], beta[4] = {0, 0, 0, 0}, d[4], e1[4], e2[4], t[4], t2[4], t3[4];
+  int64_t k;
+  memcpy(rt, r, vb);
+  memcpy(p, r, vb);
+  vdot(K, n, rt, r, rho);
+  for (k = 1; k <= max_iters; ++k) {
+    if (kr_tiny(orc_to_double(K, rho), c->floor)) KR_BREAK(3, k - 1);
+    kr_apply(c, p, ap);
+    vdot(K, n, rt, ap, sigma);
+    if (kr_tiny(orc_to_double(K, sigma), c->floor)) KR_BREAK(5, k - 1);
+    orc_div(K, rho, sigma, alpha);
+    for (int64_t i = 0; i < n; ++i) { /* y = (t_prev - r) + alpha (Ap - w) */
+      orc_sub(K, tp + i * K, r + i * K, t);
+      orc_sub(K, ap + i * K, w + i * K, t2);
+      orc_mul(K, alpha, t2, t3);
+      orc_add(K, t, t3, y + i * K);
+    }
+    kr_neg(K, alpha, ma);
+    memcpy(tv, r, vb);
+    kr_axpy(K, n, ma, ap, tv);
+    kr_norm2(K, n, tv, tn);
+    if (kr_le(K, tn, c->thr)) { /* half step converged (krylov.hpp:507-515) */
+      kr_axpy(K, n, alpha, p, x);
+      memcpy(r, tv, vb);
+      c->hist[c->nh++] = orc_to_double(K, tn);
+      *status = 0;
+      *reason = 0;
+      *iters = k;
+      goto out;
+    }
+    kr_apply(c, tv, at);
+    vdot(K, n, at, tv, att);
+    vdot(K, n, at, at, ata);
+    if (k == 1) {
+      if (kr_tiny(orc_to_double(K, ata), c->floor)) KR_BREAK(8, k - 1);
+      orc_div(K, att, ata, zeta);
+      for (int j = 0; j < K; ++j) eta[j] = 0.0;
+    } else {
+      vdot(K, n, y, y, yy);
+      vdot(K, n, y, at, yat);
+      vdot(K, n, y, tv, yt);
+      orc_mul(K, ata, yy, e1);
+      orc_mul(K, yat, yat, e2);
+      orc_sub(K, e1, e2, d);
+      if (kr_tiny(orc_to_double(K, d), c->floor * c->floor)) KR_BREAK(9, k - 1);
+      orc_mul(K, yy, att, e1);
+      orc_mul(K, yt, yat, e2);
+      orc_sub(K, e1, e2, t);
+      orc_div(K, t, d, zeta);
+      orc_mul(K, ata, yt, e1);
+      orc_mul(K, yat, att, e2);
+      orc_sub(K, e1, e2, t);
+      orc_div(K, t, d, eta);
+    }
+    for (int64_t i = 0; i < n; ++i) { /* u = zeta Ap + eta ((t_prev - r) + beta u) */
+      orc_sub(K, tp + i * K, r + i * K, t);
+      orc_mul(K, beta, u + i * K, t2);
+      orc_add(K, t, t2, t3);
+      orc_mul(K, eta, t3, t);
+      orc_mul(K, zeta, ap + i * K, t2);
+      orc_add(K, t2, t, u + i * K);
+    }
+    for (int64_t i = 0; i < n; ++i) { /* z = (zeta r + eta z) - alpha u */
+      orc_mul(K, zeta, r + i * K, t);
+      orc_mul(K, eta, z + i * K, t2);
+      orc_add(K, t, t2, t3);
+      orc_mul(K, alpha, u + i * K, t);
+      orc_sub(K, t3, t, z + i * K);
+    }
+    kr_axpy(K, n, alpha, p, x);
+    for (int64_t i = 0; i < n; ++i) orc_add(K, x + i * K, z + i * K, x + i * K);
+    memcpy(r, tv, vb); /* r = t - eta y - zeta At */
+    kr_neg(K, eta, me);
+    kr_neg(K, zeta, mz);
+    kr_axpy(K, n, me, y, r);
+    kr_axpy(K, n, mz, at, r);
+    kr_norm2(K, n, r, rn);
+    KR_RECORD(rn);
+    vdot(K, n, rt, r, rho_next);
+    if (kr_tiny(orc_to_double(K, zeta), c->floor)) KR_BREAK(10, k);
+    orc_div(K, alpha, zeta, e1);
+    orc_div(K, rho_next, rho, e2);
+    orc_mul(K, e1, e2, beta);
+    for (int64_t i = 0; i < n; ++i) { /* w = At + beta Ap; p = r + beta (p - u) */
+      orc_mul(K, beta, ap + i * K, t);
+      orc_add(K, at + i * K, t, w + i * K);
+      orc_sub(K, p + i * K, u + i * K, t);
+      orc_mul(K, beta, t, t2);
+      orc_add(K, r + i * K, t2, p + i * K);
+    }
+    memcpy(tp, tv, vb);
+    memcpy(rho, rho_next, sizeof(rho));
+  }
+  *status = 1;
+  *iters = max_iters;
+out:
+  free(rt);
+  free(p);
+  free(tp);
+  free(w);
+  free(u);
+  free(z);
+  free(y);
+  free(ap);
+  free(tv);
+  free(at);
+}
+
+/* solve() (krylov.hpp:596-606).  x0 may be NULL (zero start).  history needs
+ * max_iters + 1 entries.  Returns the history length, or -1 on a config error
+ * (SolverConfig::validate, krylov.hpp:69-75). */
+ORC_API int orc_solve(int method, int K, int lanes, int threads, int64_t n, const int64_t *indptr,
+                      const int64_t *indices, const double *vals, const double *b, const double *x0,
+                      double rel_tol, double abs_tol, int64_t max_iters, double *x, double *history,
+                      int64_t *iterations, int *status, int *reason, double *rhs_norm,
+                      double *final_true_residual) {
+  if (!(rel_tol > 0.0) || !(abs_tol > 0.0) || max_iters < 1 || method < 0 || method > 4) return -1;
+  KrCtx c = {K, lanes, threads < 1 ? 1 : threads, n, indptr, indices, vals, {0, 0, 0, 0}, 0, 0, history, 0};
+  KR_VEC(r);
+  KR_VEC(q);
+  double t[4], bn[4], tmp[4], r0[4];
+  for (int64_t i = 0; i < n * K; ++i) x[i] = 0.0;
+  if (x0) { /* x = scalar_like(x0); r = b - A x (krylov.hpp:174-181) */
+    for (int64_t i = 0; i < n; ++i) x[i * K] = x0[i];
+    kr_apply(&c, x, q);
+    for (int64_t i = 0; i < n; ++i) orc_sub(K, b + i * K, q + i * K, r + i * K);
+  } else {
+    memcpy(r, b, sizeof(double) * (size_t)(n * K));
+  }
+  kr_norm2(K, n, b, bn);
+  orc_mul_d(K, bn, rel_tol, tmp);
+  double at[4] = {abs_tol, 0, 0, 0};
+  orc_add(K, tmp, at, c.thr);
+  *rhs_norm = orc_to_double(K, bn);
+  c.cap = 1e6 * *rhs_norm + 1e6 * abs_tol;
+  c.floor = 1e-3 * abs_tol;
+  kr_norm2(K, n, r, r0);
+  history[c.nh++] = orc_to_double(K, r0);
+  *reason = 0;
+  if (kr_le(K, r0, c.thr)) {
+    *status = 0;
+    *iterations = 0;
+  } else {
+    void (*fn[5])(KrCtx *, double *, double *, int64_t, int64_t *, int *, int *) = {
+        kr_cg, kr_bicg, kr_cgs, kr_bicgstab, kr_gpbicg};
+    fn[method](&c, x, r, max_iters, iterations, status, reason);
+  }
+  kr_apply(&c, x, q); /* finish_true_residual */
+  for (int64_t i = 0; i < n; ++i) orc_sub(K, b + i * K, q + i * K, q + i * K);
+  kr_norm2(K, n, q, t);
+  *final_true_residual = orc_to_double(K, t);
+  free(r);
+  free(q);
+  return (int)c.nh;
+}

@@ -380,6 +380,53 @@ int64_t ref_cg(void* A, void* b, int lanes, int threads, double rel_tol, double 
   return rc == 0 ? written : -1;
 }
 
+// ---- solve() (krylov.hpp:596-606): every KrylovMethod through CsrOperator --
+// method: KrylovMethod order (CG, BiCG, CGS, BiCGSTAB, GPBiCG); x0 NULL = zero.
+int64_t ref_solve(void* A, void* b, int method, int lanes, int threads, double rel_tol, double abs_tol,
+                  int64_t max_iters, const double* x0, double* x_out, double* history, int64_t hist_cap,
+                  int64_t* iterations, int* status, double* rhs_norm, double* final_true, double* final_rec,
+                  char* detail, int detail_cap) {
+  auto* a = static_cast<CsrH*>(A);
+  auto* bv = static_cast<VecH*>(b);
+  int64_t written = -1;
+  int rc = guard([&] {
+    std::visit(
+        [&](auto& mat, auto& vec) {
+          using E = std::decay_t<decltype(mat.values.get(0))>;
+          using F = typename std::decay_t<decltype(vec)>::value_type;
+          if constexpr (std::is_same_v<E, F>) {
+            CsrOperator<E> op{&mat, threads, lanes != 0};
+            SolverConfig cfg;
+            cfg.method = static_cast<KrylovMethod>(method);
+            cfg.rel_tol = rel_tol;
+            cfg.abs_tol = abs_tol;
+            cfg.max_iters = max_iters;
+            cfg.threads = threads;
+            cfg.lanes_enabled = lanes != 0;
+            if (x0) cfg.x0.assign(x0, x0 + vec.size());
+            auto res = solve(op, vec, cfg);
+            read_vec(res.x, x_out);
+            int64_t n = static_cast<int64_t>(res.report.residual_history.size());
+            written = n < hist_cap ? n : hist_cap;
+            for (int64_t i = 0; i < written; ++i) history[i] = res.report.residual_history[i];
+            *iterations = res.report.iterations;
+            *status = static_cast<int>(res.report.status);
+            *rhs_norm = res.report.rhs_norm;
+            *final_true = res.report.final_true_residual;
+            *final_rec = res.report.final_recurrence_residual;
+            if (detail_cap > 0) {
+              std::strncpy(detail, res.report.detail.c_str(), static_cast<size_t>(detail_cap - 1));
+              detail[detail_cap - 1] = 0;
+            }
+          } else {
+            throw std::runtime_error("ref_solve: precision mismatch");
+          }
+        },
+        a->m, bv->v);
+  });
+  return rc == 0 ? written : -1;
+}
+
 // ---- reference test fixtures (tests/support/fixtures.hpp) ---------------
 // name: "example5x5", "tub1000", "qc324_re", "qc324_im", "random_coo" (seed,
 // nrows, ncols, nnz), "diag_dominant_sym" (seed, n, density*1e6).

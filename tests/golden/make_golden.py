@@ -213,6 +213,20 @@ def mixed_sptmv():
     return out
 
 
+def krylov_small():
+    """The reference solve() (all five methods) on tests.util.krylov_cases()."""
+    from tests.util import krylov_cases
+
+    out = {}
+    for name, A, b, m, kw in krylov_cases():
+        r = O.ref_solve(A, b, m, **kw)
+        out[f"{name}_history"] = r["history"]
+        out[f"{name}_x"] = r["x"]
+        out[f"{name}_meta"] = np.array([r["iterations"], r["status"], r["rhs_norm"], r["final_true_residual"]])
+        out[f"{name}_detail"] = np.array(r["detail"])
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cg-full", action="store_true")
@@ -220,7 +234,7 @@ def main():
     a = ap.parse_args()
     assert O.ref_available(), "build the reference first: make -C oracle ref"
     jobs = {"arith": arith, "spmv_small": spmv_small, "spmv_full": spmv_full, "cg_small": cg_small,
-            "mixed_sptmv": mixed_sptmv}
+            "mixed_sptmv": mixed_sptmv, "krylov_small": krylov_small}
     if a.cg_full:
         jobs = {"cg_full": cg_full}
     for name, fn in jobs.items():

@@ -228,3 +228,55 @@ def test_sptmv_single_thread_equals_spmv_of_transpose():
     A = synth.config_matrix(2, 2, 700, 16.0)
     v = synth.config_vector(2, A.nrows, 2)
     assert O.sptmv(A, v).tobytes() == O.spmv(transpose(A), v, 0).tobytes()
+
+
+# ---- Krylov solvers (krylov.hpp:238-606): the C restatement vs the reference ----
+from tests.util import BREAKDOWN_CASES, krylov_cases  # noqa: E402
+
+_KCASES = krylov_cases()
+
+
+@pytest.mark.parametrize("case", _KCASES, ids=[c[0] for c in _KCASES])
+def test_oracle_solvers_equal_reference_golden(case):
+    """Every method, bit for bit: iterate, residual history, iteration count,
+    status, detail text and final true residual (golden from the reference's
+    own solve(), tests/golden/make_golden.py krylov_small)."""
+    name, A, b, m, kw = case
+    g = golden("krylov_small")
+    r = O.solve(A, b, m, **kw)
+    meta = g[f"{name}_meta"]
+    assert bits_equal(r["history"], g[f"{name}_history"])
+    assert bits_equal(r["x"], g[f"{name}_x"])
+    assert (r["iterations"], r["status"]) == (int(meta[0]), int(meta[1]))
+    assert bits_equal(np.array([r["rhs_norm"], r["final_true_residual"]]), meta[2:])
+    assert r["detail"] == str(g[f"{name}_detail"])
+
+
+def test_breakdown_cases_cover_every_exit():
+    details = {d for _, _, _, d in BREAKDOWN_CASES}
+    assert len(details) == len(BREAKDOWN_CASES)
+    g = golden("krylov_small")
+    for i, (m, _, _, d) in enumerate(BREAKDOWN_CASES):
+        assert str(g[f"breakdown{i}_{m}_detail"]) == d
+        assert int(g[f"breakdown{i}_{m}_meta"][1]) == 2  # SolverStatus::Breakdown
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="live reference not built on this host")
+@pytest.mark.parametrize("m", O.METHODS)
+@pytest.mark.parametrize("threads", [1, 4])
+def test_oracle_solvers_equal_live_reference(m, threads):
+    from tests.util import krylov_system
+
+    A, b = krylov_system(50, 2, seed=17, symmetric=m == "cg", density=0.15)
+    r1 = O.solve(A, b, m, threads=threads, order=0)
+    r2 = O.ref_solve(A, b, m, threads=threads, order=0)
+    assert bits_equal(r1["history"], r2["history"]) and bits_equal(r1["x"], r2["x"])
+    assert (r1["iterations"], r1["status"], r1["detail"]) == (r2["iterations"], r2["status"], r2["detail"])
+
+
+def test_oracle_solver_rejects_bad_config():
+    A, b = krylov_cases()[0][1:3]
+    with pytest.raises(ValueError):
+        O.solve(A, b, "cg", rel_tol=0.0)
+    with pytest.raises(ValueError):
+        O.solve(A, b, "cg", max_iters=0)

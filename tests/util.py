@@ -104,3 +104,100 @@ def transpose(A):
     planes = np.ascontiguousarray(np.asarray(A.planes)[:, perm])
     return SimpleNamespace(nrows=A.ncols, ncols=A.nrows, indptr=tptr, indices=rows[perm], planes=planes,
                            K=getattr(A, "K", None), nnz=len(perm))
+
+
+def krylov_system(n, K, seed=0, symmetric=False, density=0.1, dominance=1.0):
+    """Seeded diagonally dominant n x n system with full-width K-component
+    values (like the reference's random_diag_dominant, tests/support/
+    fixtures.hpp) and a right-hand side b; test-side generator."""
+    import synth
+
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n, n)) < density
+    if symmetric:
+        mask = np.triu(mask, 1)
+        mask = mask | mask.T
+    np.fill_diagonal(mask, True)
+    rows = [np.nonzero(mask[i])[0].tolist() for i in range(n)]
+    A = csr(n, n, rows, K, seed=seed + 1)
+    hi = A.planes[0]
+    if symmetric:  # mirror the values of the upper triangle
+        pos = {}
+        for i in range(n):
+            for k in range(A.indptr[i], A.indptr[i + 1]):
+                pos[(i, int(A.indices[k]))] = k
+        for (i, j), k in pos.items():
+            if j < i:
+                A.planes[:, k] = A.planes[:, pos[(j, i)]]
+    for i in range(n):
+        lo, hi_ = A.indptr[i], A.indptr[i + 1]
+        off = [k for k in range(lo, hi_) if A.indices[k] != i]
+        d = [k for k in range(lo, hi_) if A.indices[k] == i][0]
+        A.planes[:, d] = 0.0
+        A.planes[0, d] = float(np.sum(np.abs(hi[off]))) * dominance + 1.0 + rng.random()
+    b = synth.vector(synth.VAL_NORMAL, n, K, seed=seed + 2)
+    return A, b
+
+
+# small integer systems that drive each solver into one of its breakdown exits
+# (found by a seeded search with the oracle; reference detail texts)
+BREAKDOWN_CASES = [
+    ("bicg", [[1, -2], [-1, 0]], [0, -2], "bicg: <p~, Ap> vanished"),
+    ("bicg", [[1, 0], [2, 2]], [-1, 0], "bicg: <r~, r> vanished"),
+    ("cgs", [[1, -2], [-1, 0]], [0, -2], "cgs: <r~, Ap> vanished"),
+    ("cgs", [[1, 0], [2, 2]], [-1, 0], "cgs: <r~, r> vanished"),
+    ("bicgstab", [[1, -2], [-1, 0]], [0, -2], "bicgstab: <r~, Ap> vanished"),
+    ("bicgstab", [[2, 2, 0], [-2, -2, 0], [-2, -2, 1]], [-1, -2, 2], "bicgstab: <r~, r> vanished"),
+    ("bicgstab", [[1, 1], [2, 2]], [2, 2], "bicgstab: <t, t> vanished"),
+    ("bicgstab", [[0, 2], [-1, -2]], [0, -2], "bicgstab: omega vanished"),
+    ("gpbicg", [[0, 2], [0, -1]], [0, 1], "gpbicg: <At, At> vanished"),
+    ("gpbicg", [[1, -2], [-1, 0]], [0, -2], "gpbicg: <r~, Ap> vanished"),
+    ("gpbicg", [[2, 2, -2], [1, 1, 2], [-1, 2, -1]], [2, 2, 0], "gpbicg: <r~, r> vanished"),
+    ("gpbicg", [[0, 2], [-1, -2]], [0, -2], "gpbicg: zeta vanished"),
+    ("gpbicg", [[1, -1], [2, -2]], [2, 1], "gpbicg: zeta/eta system is singular"),
+    ("cg", [[0, 1], [-1, 0]], [1, 1], "cg: <p, Ap> vanished"),
+]
+
+
+def dense_system(M, bvec, K=2):
+    """Integer dense matrix / rhs -> K-component CSR + AoS rhs (zero tails)."""
+    M = np.asarray(M, float)
+    n = M.shape[0]
+    rows = [[j for j in range(n) if M[i, j] != 0] for i in range(n)]
+    vals = np.array([M[i, j] for i in range(n) for j in rows[i]])
+    planes = np.zeros((K, len(vals)))
+    planes[0] = vals
+    b = np.zeros((n, K))
+    b[:, 0] = bvec
+    return csr(n, n, rows, K, planes=planes), b
+
+
+def krylov_cases():
+    """(name, A, b, method, kwargs) parity cases shared by the oracle golden, the
+    oracle tests and the device tests."""
+    out = []
+    for sym in (True, False):
+        for K in (2, 3, 4):
+            A, b = krylov_system(60, K, seed=3, symmetric=sym)
+            for m in ("cg", "bicg", "cgs", "bicgstab", "gpbicg"):
+                if m == "cg" and not sym:
+                    continue
+                out.append((f"{'sym' if sym else 'nonsym'}_K{K}_{m}", A, b, m, {}))
+    A, b = krylov_system(60, 2, seed=3, symmetric=False)
+    out.append(("nonsym_K2_bicg_t3", A, b, "bicg", {"threads": 3}))
+    A, b = krylov_system(40, 3, seed=5, symmetric=False, dominance=0.2)
+    for m in ("bicg", "cgs", "bicgstab", "gpbicg"):
+        out.append((f"weak_K3_{m}", A, b, m, {"max_iters": 300}))
+    A, b = krylov_system(30, 4, seed=9, symmetric=True)
+    for m in ("cg", "bicg", "cgs", "bicgstab", "gpbicg"):
+        out.append((f"maxit_K4_{m}", A, b, m, {"rel_tol": 1e-60, "max_iters": 15}))
+    I, bi = dense_system(np.eye(6), [0.5, -1.25, 2.0, 3.5, -0.75, 1.0])
+    D, bd = dense_system(np.diag([1.0, 2.0, 4.0]), [1.0, 4.0, 16.0])
+    for m in ("cg", "bicg", "cgs", "bicgstab", "gpbicg"):
+        out.append((f"identity_{m}", I, bi, m, {}))
+        out.append((f"x0exact_{m}", D, bd, m, {"x0": [1.0, 2.0, 4.0]}))
+        out.append((f"x0_{m}", D, bd, m, {"x0": [0.5, -1.0, 3.0]}))
+    for i, (m, M, bv, _) in enumerate(BREAKDOWN_CASES):
+        A, b = dense_system(M, bv)
+        out.append((f"breakdown{i}_{m}", A, b, m, {"max_iters": 50}))
+    return out
