@@ -13,6 +13,8 @@
  *   spmv_complex<E,F>(A, v, KernelMode) (kernels.hpp:399)   mpsg_spmv_complex(_dev)
  *   CsrOperator<E>::apply (krylov.hpp:101-120)              mpsg_spmv_dev (operator seam)
  *   solve_cg<E,Op>(op, b, SolverConfig) (krylov.hpp:238)    mpsg_cg
+ *   solve<E,Op>(op, b, SolverConfig) (krylov.hpp:596-606)   mpsg_solve
+ *     (solve_bicg / _cgs / _bicgstab / _gpbicg, :283-594)
  *   detail::partition_rows (kernels.hpp:63-80)              mpsg_partition_rows
  *   checksum (bench.hpp:113-150)                            mpsg_checksum(_complex)
  *
@@ -85,6 +87,22 @@ enum mpsg_solver_status {
   MPSG_DIVERGED = 3
 };
 
+/* KrylovMethod, krylov.hpp:24 (same order) */
+enum mpsg_method {
+  MPSG_CG = 0,
+  MPSG_BICG = 1,
+  MPSG_CGS = 2,
+  MPSG_BICGSTAB = 3,
+  MPSG_GPBICG = 4
+};
+
+/* Dot-product order of the device solvers. */
+enum mpsg_dot_order {
+  MPSG_DOT_TREE = 0,       /* fixed-shape parallel tree: deterministic, not the reference's bits */
+  MPSG_DOT_SEQUENTIAL = 1  /* one thread, i ascending: the reference's dot (krylov.hpp:122-128);
+                              with an exact SpMV order the solve reproduces the reference bit for bit */
+};
+
 /* mpsg_csr_upload_ex flags */
 enum mpsg_csr_flags {
   MPSG_CSR_COMPLEX = 1,   /* 2x the planes: re then im over one structure (ComplexSparseMatrix) */
@@ -118,6 +136,19 @@ typedef struct mpsg_cg_config {
   int32_t check_every; /* host polls the device status every N iterations (0 = 32) */
   int32_t use_graph;   /* capture the iteration batch in a CUDA graph (default 1) */
 } mpsg_cg_config;
+
+/* SolverConfig (krylov.hpp:58-75) for mpsg_solve. */
+typedef struct mpsg_solver_config {
+  int32_t method;      /* mpsg_method (the reference default is BiCGSTAB) */
+  int32_t threads;     /* KernelMode::threads of the operator: BiCG's sptmv merge order */
+  double rel_tol;      /* default 1e-13 */
+  double abs_tol;      /* default 1e-99 */
+  int64_t max_iters;   /* default 10000 */
+  int32_t check_every; /* host polls the device status every N iterations (0 = 32) */
+  int32_t use_graph;   /* capture the iteration batch in a CUDA graph (default 1) */
+  int32_t dot_order;   /* mpsg_dot_order */
+  int32_t reserved;
+} mpsg_solver_config;
 
 /* SolverReport (krylov.hpp:77-88). */
 typedef struct mpsg_cg_report {
@@ -204,6 +235,16 @@ MPSG_API int mpsg_sptmv_complex_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order,
 MPSG_API int mpsg_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, const double* b,
             const double* x0, const mpsg_cg_config* cfg, double* x_out, double* history,
             int64_t history_cap, mpsg_cg_report* report);
+
+/* ---- solve() (krylov.hpp:596-606): CG, BiCG, CGS, BiCGSTAB, GPBiCG --- */
+/* Device-resident Krylov solve of A x = b (real, square), the method chosen
+ * by cfg->method; the reference solver's breakdown / divergence / half-step
+ * exits, iteration counts, residual history and final true residual.  BiCG
+ * needs the transpose (MPSG_CSR_TRANSPOSE).  Arguments as mpsg_cg; the
+ * report's detail is the reference text ("bicgstab: omega vanished", ...). */
+MPSG_API int mpsg_solve(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, const double* b,
+                        const double* x0, const mpsg_solver_config* cfg, double* x_out, double* history,
+                        int64_t history_cap, mpsg_cg_report* report);
 
 /* ---- row-sharded multi-GPU (one process per GPU, NCCL) ------------------ */
 /* Rank r owns rows [bounds[r], bounds[r+1]) (mpsg_partition_rows gives the

@@ -16,6 +16,10 @@ argument meaning and error behaviour follow the reference
   CsrOperator (krylov.hpp:101-120)             CsrOperator
   SolverConfig / SolverReport (krylov.hpp)     SolverConfig / SolverReport
   solve_cg(op, b, cfg) (krylov.hpp:238)        solve_cg(op, b, cfg)
+  solve(op, b, cfg) (krylov.hpp:596-606)       solve(op, b, cfg) -- cfg.method picks
+  solve_bicg/cgs/bicgstab/gpbicg (:283-594)    solve_bicg / solve_cgs / solve_bicgstab /
+                                               solve_gpbicg (device-resident)
+  KrylovMethod / parse_method (krylov.hpp:24)  KrylovMethod / parse_method
   partition_rows (kernels.hpp:63-80)           partition_rows
   checksum (bench.hpp:113-150)                 checksum / checksum_complex
 
@@ -63,6 +67,12 @@ class _CgConfig(ctypes.Structure):
                 ("check_every", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
 
 
+class _SolverConfig(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int32), ("threads", ctypes.c_int32), ("rel_tol", _f64), ("abs_tol", _f64),
+                ("max_iters", _i64), ("check_every", ctypes.c_int32), ("use_graph", ctypes.c_int32),
+                ("dot_order", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 class _CgReport(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("converged", ctypes.c_int32), ("iterations", _i64),
                 ("history_len", _i64), ("rhs_norm", _f64), ("final_recurrence_residual", _f64),
@@ -82,7 +92,7 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
            "mpsg_dcg", "mpsg_halo_plan", "mpsg_csr_upload_ex", "mpsg_sptmv", "mpsg_sptmv_dev",
            "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local", "mpsg_make_vector",
-           "mpsg_sptmv_ex", "mpsg_sptmv_complex_ex")
+           "mpsg_sptmv_ex", "mpsg_sptmv_complex_ex", "mpsg_solve")
 
 CSR_COMPLEX, CSR_MIXED, CSR_TRANSPOSE = 1, 2, 4
 
@@ -113,6 +123,8 @@ def lib():
     L.mpsg_spmv_complex_dev.argtypes = [_P, _P, _i32, _P, _P, _P, _P, _P]
     L.mpsg_cg.argtypes = [_P, _P, _i32, _i64, _P, _P, ctypes.POINTER(_CgConfig), _P, _P, _i64,
                           ctypes.POINTER(_CgReport)]
+    L.mpsg_solve.argtypes = [_P, _P, _i32, _i64, _P, _P, ctypes.POINTER(_SolverConfig), _P, _P, _i64,
+                             ctypes.POINTER(_CgReport)]
     L.mpsg_partition_rows.argtypes = [_P, _i64, _i32, _P]
     L.mpsg_checksum.argtypes = [_i32, _i64, _P]
     L.mpsg_checksum.restype = _u64
@@ -360,8 +372,28 @@ class SolverStatus(enum.IntEnum):  # krylov.hpp:46
     Diverged = 3
 
 
+class KrylovMethod(enum.IntEnum):  # krylov.hpp:24
+    CG = 0
+    BiCG = 1
+    CGS = 2
+    BiCGSTAB = 3
+    GPBiCG = 4
+
+    def __str__(self):  # to_string (krylov.hpp:26-35)
+        return ("cg", "bicg", "cgs", "bicgstab", "gpbicg")[int(self)]
+
+
+def parse_method(s: str) -> Optional[KrylovMethod]:  # krylov.hpp:37-44
+    return {"cg": KrylovMethod.CG, "bicg": KrylovMethod.BiCG, "cgs": KrylovMethod.CGS,
+            "bicgstab": KrylovMethod.BiCGSTAB, "gpbicg": KrylovMethod.GPBiCG}.get(s)
+
+
+DOT_TREE, DOT_SEQUENTIAL = 0, 1
+
+
 @dataclass
-class SolverConfig:  # krylov.hpp:58-75 (CG subset)
+class SolverConfig:  # krylov.hpp:58-75
+    method: KrylovMethod = KrylovMethod.BiCGSTAB
     rel_tol: float = 1e-13
     abs_tol: float = 1e-99
     max_iters: int = 10000
@@ -371,6 +403,9 @@ class SolverConfig:  # krylov.hpp:58-75 (CG subset)
     x0: Sequence[float] | None = None
     check_every: int = 32
     use_graph: bool = True
+    # reference dot order (one device thread per dot, krylov.hpp:122-128): with
+    # an exact SpMV order the device solve reproduces the reference's bits
+    exact_dots: bool = False
 
     def validate(self):
         if not (self.rel_tol > 0.0) or not (self.abs_tol > 0.0):
@@ -458,6 +493,63 @@ def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult
         final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
         solve_seconds=rep.solve_seconds, device_seconds=rep.device_seconds)
     return SolveResult(x, report)
+
+
+def _solve_method(op: CsrOperator, b, cfg: SolverConfig, method) -> SolveResult:
+    cfg.validate()
+    A = op.matrix
+    bb = _aos(b, "solver")
+    if op.rows() != op.cols():
+        raise ValueError(f"solver: operator must be square, got {op.rows()}x{op.cols()}")
+    if bb.shape[0] != op.cols():
+        raise ValueError("solver: rhs length does not match the operator")
+    x0 = None
+    if cfg.x0 is not None and len(cfg.x0) > 0:
+        if len(cfg.x0) != bb.shape[0]:
+            raise ValueError("solver: x0 length does not match the rhs")
+        x0 = np.zeros_like(bb)
+        x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)  # scalar_like (krylov.hpp:178)
+    c = _SolverConfig(int(method), max(op.threads, 1), cfg.rel_tol, cfg.abs_tol, cfg.max_iters,
+                      cfg.check_every, 1 if cfg.use_graph else 0,
+                      DOT_SEQUENTIAL if cfg.exact_dots else DOT_TREE, 0)
+    rep = _CgReport()
+    x = np.empty_like(bb)
+    hist = np.empty(cfg.max_iters + 1)
+    order = ORDER_FAST if (cfg.fast or op.fast) else (ORDER_LANE4 if (cfg.lanes_enabled and op.lanes_enabled)
+                                                       else ORDER_SCALAR)
+    A.ctx.check(lib().mpsg_solve(A.ctx.h, A.h, order, bb.shape[0], _p(bb), _p(x0), ctypes.byref(c), _p(x),
+                                 _p(hist), len(hist), ctypes.byref(rep)))
+    report = SolverReport(
+        status=SolverStatus(rep.status), converged=bool(rep.converged), detail=rep.detail.decode(),
+        iterations=int(rep.iterations), residual_history=hist[: rep.history_len].tolist(),
+        rhs_norm=rep.rhs_norm, final_recurrence_residual=rep.final_recurrence_residual,
+        final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
+        solve_seconds=rep.solve_seconds, device_seconds=rep.device_seconds)
+    return SolveResult(x, report)
+
+
+def solve(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:
+    """solve() (krylov.hpp:596-606): the device-resident Krylov method
+    cfg.method (CG, BiCG, CGS, BiCGSTAB, GPBiCG).  BiCG needs a matrix
+    uploaded with ``transpose=True``."""
+    cfg = cfg or SolverConfig()
+    return _solve_method(op, b, cfg, cfg.method)
+
+
+def solve_bicg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:283
+    return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.BiCG)
+
+
+def solve_cgs(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:337
+    return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.CGS)
+
+
+def solve_bicgstab(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:398
+    return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.BiCGSTAB)
+
+
+def solve_gpbicg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:492
+    return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.GPBiCG)
 
 
 # --------------------------------------------------------------------------- multi-GPU

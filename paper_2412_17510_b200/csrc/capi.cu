@@ -642,14 +642,17 @@ int mpsg_sptmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_
   return launch_spmv(ctx, T, torder(order), d_v, nullptr, d_y, nullptr, st);
 }
 
+}  // extern "C"
+
 namespace {
-// Segment bounds of the reference's T-thread sptmv (partition_rows of A) for
-// the launch that follows; cleared again by SegScope's destructor.
+// Clears the segment bounds set for one transposed launch.
 struct SegScope {
   mpsg_ctx* ctx;
   ~SegScope() { ctx->seg_T = 1; }
 };
-int set_segments(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads) {
+}  // namespace
+
+int mpsg::set_segments(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads) {
   ctx->seg_T = 1;
   if (threads <= 1 || order == MPSG_ORDER_FAST || A->nrows == 0) return MPSG_OK;
   ctx->seg_host.assign((size_t)threads + 1, 0);
@@ -666,7 +669,8 @@ int set_segments(mpsg_ctx* ctx, const mpsg_csr* A, int order, int threads) {
   ctx->seg_T = threads;
   return MPSG_OK;
 }
-}  // namespace
+
+extern "C" {
 
 int mpsg_sptmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t vlen, const double* v, double* y) {
   return mpsg_sptmv_ex(ctx, A, order, 1, vlen, v, y);
@@ -767,6 +771,34 @@ int mpsg_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, const dou
     case 4: return run_cg<4>(ctx, A, order, b, x0, cfg, x_out, history, history_cap, report);
   }
   return fail(ctx, MPSG_E_ARG, "cg: unsupported K");
+}
+
+int mpsg_solve(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, const double* b, const double* x0,
+               const mpsg_solver_config* cfg, double* x_out, double* history, int64_t history_cap,
+               mpsg_cg_report* report) {
+  if (!ctx || !A || !cfg || !report || !b) return MPSG_E_ARG;
+  // SolverConfig::validate (krylov.hpp:69-75) and solver_init shape checks (:164-176)
+  if (!(cfg->rel_tol > 0.0) || !(cfg->abs_tol > 0.0))
+    return fail(ctx, MPSG_E_ARG, "solver: tolerances must be positive");
+  if (cfg->max_iters < 1) return fail(ctx, MPSG_E_ARG, "solver: max_iters must be at least 1");
+  if (cfg->threads < 1) return fail(ctx, MPSG_E_ARG, "solver: threads must be at least 1");
+  if (cfg->method < MPSG_CG || cfg->method > MPSG_GPBICG)
+    return fail(ctx, MPSG_E_ARG, "solve: unknown method %d", cfg->method);
+  if (cfg->dot_order != MPSG_DOT_TREE && cfg->dot_order != MPSG_DOT_SEQUENTIAL)
+    return fail(ctx, MPSG_E_ARG, "solve: unknown dot order %d", cfg->dot_order);
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "solver: complex matrices are not supported");
+  if (A->nrows != A->ncols)
+    return fail(ctx, MPSG_E_DIM, "solver: operator must be square, got %lldx%lld", (long long)A->nrows,
+                (long long)A->ncols);
+  if (blen != A->ncols) return fail(ctx, MPSG_E_DIM, "solver: rhs length does not match the operator");
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "solve: unknown order %d", order);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  switch (A->K) {
+    case 2: return krylov_driver<2>(ctx, A, cfg, order, b, x0, x_out, history, history_cap, report);
+    case 3: return krylov_driver<3>(ctx, A, cfg, order, b, x0, x_out, history, history_cap, report);
+    case 4: return krylov_driver<4>(ctx, A, cfg, order, b, x0, x_out, history, history_cap, report);
+  }
+  return fail(ctx, MPSG_E_ARG, "solve: unsupported K");
 }
 
 int mpsg_partition_rows(const int64_t* indptr, int64_t nrows, int parts, int64_t* bounds) {
