@@ -14,6 +14,10 @@
 //   mps::sptmv_complex(..., bool conjugate) kernels.hpp:419 mps::gpu::sptmv_complex (same)
 //   mps::CsrOperator<E> (Op concept)    krylov.hpp:101     mps::gpu::GpuCsrOperator<E>
 //   mps::solve_cg(op, b, cfg)           krylov.hpp:238     mps::gpu::solve_cg (device-resident)
+//   mps::solve(op, b, cfg) and          krylov.hpp:596     mps::gpu::solve / solve_bicg / solve_cgs /
+//     solve_bicg/cgs/bicgstab/gpbicg    krylov.hpp:283-594   solve_bicgstab / solve_gpbicg (device-
+//                                                            resident; DotOrder::Sequential = the
+//                                                            reference's bits)
 //                                                          -- or the reference's own solvers
 //                                                          (solve_cg, solve_bicg, ...) with a
 //                                                          GpuCsrOperator (same Op concept)
@@ -357,7 +361,7 @@ inline std::vector<std::int64_t> partition_rows(const std::vector<std::int64_t>&
 template <class MatE, class VecE = MatE>
 struct GpuCsrOperator {
   const DeviceCsr<MatE, VecE>* matrix = nullptr;
-  int threads = 1;  // ignored on the device (kept for the reference's shape)
+  int threads = 1;  // apply_transposed / BiCG: the reference sptmv's per-thread merge order
   bool lanes_enabled = true;
   bool fast = false;
 
@@ -375,40 +379,28 @@ struct GpuCsrOperator {
   }
 };
 
-// Device-resident CG (krylov.hpp:238-281): vectors and scalars never leave
-// the GPU; the residual history, status and true residual come back in the
-// reference's SolverReport.  Only rel_tol, abs_tol, max_iters, x0 and
-// lanes_enabled of SolverConfig are read (as by the reference CG).  Pure mode.
-template <class E>
-SolveResult<E> solve_cg(const GpuCsrOperator<E, E>& op, const std::vector<E>& b, const SolverConfig& cfg) {
-  constexpr int K = detail::mc_width<E>::value;
-  static_assert(K >= 2, "device CG runs on MultiComponent<K>");
+namespace detail {
+template <class MatE, class E>
+void check_solve_args(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg,
+                      std::vector<E>& x0) {
   cfg.validate();  // krylov.hpp:69-75
   if (op.rows() != op.cols())
     throw std::invalid_argument("solver: operator must be square, got " + std::to_string(op.rows()) + "x" +
                                 std::to_string(op.cols()));
   if (static_cast<std::size_t>(op.cols()) != b.size())
     throw std::invalid_argument("solver: rhs length does not match the operator");
-  std::vector<E> x0;
   if (!cfg.x0.empty()) {
     if (cfg.x0.size() != b.size()) throw std::invalid_argument("solver: x0 length does not match the rhs");
     x0.resize(b.size());
     for (std::size_t i = 0; i < b.size(); ++i) x0[i] = E(cfg.x0[i]);  // scalar_like (krylov.hpp:178)
   }
-  mpsg_cg_config c{cfg.rel_tol, cfg.abs_tol, cfg.max_iters, 32, 1};
-  mpsg_cg_report rep{};
-  SolveResult<E> res;
-  res.x.resize(b.size());
-  std::vector<double> hist(static_cast<std::size_t>(cfg.max_iters) + 1);
-  const int order = op.fast ? MPSG_ORDER_FAST
-                            : (cfg.lanes_enabled && op.lanes_enabled ? MPSG_ORDER_LANE4 : MPSG_ORDER_SCALAR);
-  Context& ctx = op.matrix->context();
-  ctx.check(mpsg_cg(ctx.get(), op.matrix->get(), order, static_cast<std::int64_t>(b.size()),
-                    reinterpret_cast<const double*>(b.data()),
-                    x0.empty() ? nullptr : reinterpret_cast<const double*>(x0.data()), &c,
-                    reinterpret_cast<double*>(res.x.data()), hist.data(), static_cast<std::int64_t>(hist.size()),
-                    &rep));
-  auto& r = res.report;
+}
+template <class MatE, class E>
+int solve_order(const GpuCsrOperator<MatE, E>& op, const SolverConfig& cfg) {
+  return op.fast ? MPSG_ORDER_FAST : (cfg.lanes_enabled && op.lanes_enabled ? MPSG_ORDER_LANE4 : MPSG_ORDER_SCALAR);
+}
+template <class E>
+void fill_report(SolverReport& r, const mpsg_cg_report& rep, const std::vector<double>& hist) {
   r.status = static_cast<SolverStatus>(rep.status);
   r.converged = rep.converged != 0;
   r.detail = rep.detail;
@@ -419,7 +411,101 @@ SolveResult<E> solve_cg(const GpuCsrOperator<E, E>& op, const std::vector<E>& b,
   r.final_true_residual = rep.final_true_residual;
   r.setup_seconds = rep.setup_seconds;
   r.solve_seconds = rep.solve_seconds;
+}
+}  // namespace detail
+
+// Device-resident CG (krylov.hpp:238-281): vectors and scalars never leave
+// the GPU; the residual history, status and true residual come back in the
+// reference's SolverReport.  Only rel_tol, abs_tol, max_iters, x0 and
+// lanes_enabled of SolverConfig are read (as by the reference CG).  Pure or
+// Mixed mode (GpuCsrOperator<double, MultiComponent<K>>, as CsrOperator<double>
+// with a multi-component rhs in the reference's solve_core, bench.cpp:550-557).
+template <class MatE, class E>
+SolveResult<E> solve_cg(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg) {
+  constexpr int K = detail::mc_width<E>::value;
+  static_assert(K >= 2, "device CG runs on MultiComponent<K>");
+  std::vector<E> x0;
+  detail::check_solve_args(op, b, cfg, x0);
+  mpsg_cg_config c{cfg.rel_tol, cfg.abs_tol, cfg.max_iters, 32, 1};
+  mpsg_cg_report rep{};
+  SolveResult<E> res;
+  res.x.resize(b.size());
+  std::vector<double> hist(static_cast<std::size_t>(cfg.max_iters) + 1);
+  Context& ctx = op.matrix->context();
+  ctx.check(mpsg_cg(ctx.get(), op.matrix->get(), detail::solve_order(op, cfg), static_cast<std::int64_t>(b.size()),
+                    reinterpret_cast<const double*>(b.data()),
+                    x0.empty() ? nullptr : reinterpret_cast<const double*>(x0.data()), &c,
+                    reinterpret_cast<double*>(res.x.data()), hist.data(), static_cast<std::int64_t>(hist.size()),
+                    &rep));
+  detail::fill_report<E>(res.report, rep, hist);
   return res;
+}
+
+// Dot-product order of the device solvers: Tree (throughput; deterministic,
+// not the reference's bits) or Sequential (the reference's serial dot,
+// krylov.hpp:122-128 -- with lanes on/off this reproduces the reference
+// solver bit for bit: iterate, history, status, detail).
+enum class DotOrder { Tree = MPSG_DOT_TREE, Sequential = MPSG_DOT_SEQUENTIAL };
+
+// Device-resident solve() (krylov.hpp:596-606) and the per-method entry
+// points (solve_bicg :283, solve_cgs :337, solve_bicgstab :398, solve_gpbicg
+// :492).  Reads method, rel_tol, abs_tol, max_iters, x0, lanes_enabled of
+// SolverConfig; BiCG's transposed products follow the operator's thread count
+// (the reference's per-thread merge) and need a DeviceCsr uploaded with the
+// transpose.  Real, Pure or Mixed mode.
+template <class MatE, class E>
+SolveResult<E> solve_method(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg,
+                            KrylovMethod method, DotOrder dots = DotOrder::Tree) {
+  constexpr int K = detail::mc_width<E>::value;
+  static_assert(K >= 2, "device solvers run on MultiComponent<K>");
+  std::vector<E> x0;
+  detail::check_solve_args(op, b, cfg, x0);
+  mpsg_solver_config c{};
+  c.method = static_cast<int32_t>(method);
+  c.threads = std::max(op.threads, 1);
+  c.rel_tol = cfg.rel_tol;
+  c.abs_tol = cfg.abs_tol;
+  c.max_iters = cfg.max_iters;
+  c.check_every = 32;
+  c.use_graph = 1;
+  c.dot_order = static_cast<int32_t>(dots);
+  mpsg_cg_report rep{};
+  SolveResult<E> res;
+  res.x.resize(b.size());
+  std::vector<double> hist(static_cast<std::size_t>(cfg.max_iters) + 1);
+  Context& ctx = op.matrix->context();
+  ctx.check(mpsg_solve(ctx.get(), op.matrix->get(), detail::solve_order(op, cfg), static_cast<std::int64_t>(b.size()),
+                       reinterpret_cast<const double*>(b.data()),
+                       x0.empty() ? nullptr : reinterpret_cast<const double*>(x0.data()), &c,
+                       reinterpret_cast<double*>(res.x.data()), hist.data(), static_cast<std::int64_t>(hist.size()),
+                       &rep));
+  detail::fill_report<E>(res.report, rep, hist);
+  return res;
+}
+template <class MatE, class E>
+SolveResult<E> solve(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg,
+                     DotOrder dots = DotOrder::Tree) {
+  return solve_method(op, b, cfg, cfg.method, dots);
+}
+template <class MatE, class E>
+SolveResult<E> solve_bicg(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg,
+                          DotOrder dots = DotOrder::Tree) {
+  return solve_method(op, b, cfg, KrylovMethod::BiCG, dots);
+}
+template <class MatE, class E>
+SolveResult<E> solve_cgs(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg,
+                         DotOrder dots = DotOrder::Tree) {
+  return solve_method(op, b, cfg, KrylovMethod::CGS, dots);
+}
+template <class MatE, class E>
+SolveResult<E> solve_bicgstab(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg,
+                              DotOrder dots = DotOrder::Tree) {
+  return solve_method(op, b, cfg, KrylovMethod::BiCGSTAB, dots);
+}
+template <class MatE, class E>
+SolveResult<E> solve_gpbicg(const GpuCsrOperator<MatE, E>& op, const std::vector<E>& b, const SolverConfig& cfg,
+                            DotOrder dots = DotOrder::Tree) {
+  return solve_method(op, b, cfg, KrylovMethod::GPBiCG, dots);
 }
 
 }  // namespace gpu

@@ -5,8 +5,14 @@
 //
 //   mpsg spmv  <file.mtx> [--precision dd|td|qd] [--mode p|m] [--lanes on|off|fast]
 //              [--threads N] [--reps R] [--transposed] [--matrix-name NAME] [--device D]
-//   mpsg solve <file.mtx> [--method cg] [--precision ...] [--mode p] [--lanes on|off|fast]
-//              [--rtol X] [--atol X] [--max-iters N] [--history FILE] [--matrix-name NAME]
+//   mpsg solve <file.mtx> [--method cg|bicg|cgs|bicgstab|gpbicg] [--precision ...] [--mode p|m]
+//              [--lanes on|off|fast] [--threads N] [--dots tree|exact] [--rtol X] [--atol X]
+//              [--max-iters N] [--history FILE] [--matrix-name NAME]
+//   (solve: the reference's solve_core, bench.cpp:550-557 -- b = A make_vector,
+//   then solve() with the CsrOperator at --threads; --method defaults to
+//   bicgstab like the reference CLI, tools/mpsparse.cpp:184.  --dots exact runs
+//   the reference's sequential dots: the record then equals the reference's
+//   for the same --threads and --lanes, bit for bit.)
 //
 // Reference workflow restated (paths under /root/reference/proj):
 //   parse_mtx            src/mtxio.cpp:85-173 (coordinate real/integer/complex/pattern;
@@ -24,6 +30,8 @@
 // and selects the reference's thread-order merge for sptmv (kernels.hpp:368-394),
 // reproduced bit for bit.  --lanes fast selects the throughput order.
 #include <algorithm>
+#include <cctype>
+#include <cerrno>
 #include <chrono>
 #include <cinttypes>
 #include <cmath>
@@ -100,22 +108,36 @@ Coo parse_mtx(const std::string& path) {
     if (!content_line(in, line, lineno))
       die("matrix market: expected " + std::to_string(nz) + " entries, found " + std::to_string(seen));
     const char* p = line.c_str();
-    char* end = nullptr;
-    const long long r = std::strtoll(p, &end, 10) - 1;
-    p = end;
-    const long long c = std::strtoll(p, &end, 10) - 1;
-    p = end;
+    // parse_index / parse_value / expect_line_end (mtxio.cpp:40-66): a number
+    // must be present and in range, nothing may follow the entry
+    auto bad = [&](const char* what) { die("matrix market, line " + std::to_string(lineno) + ": " + what); };
+    auto index = [&]() -> long long {
+      errno = 0;
+      char* end = nullptr;
+      const long long v = std::strtoll(p, &end, 10);
+      if (end == p || errno == ERANGE) bad("expected integer");
+      p = end;
+      return v;
+    };
+    auto value = [&]() -> double {
+      errno = 0;
+      char* end = nullptr;
+      const double v = std::strtod(p, &end);
+      if (end == p || errno == ERANGE) bad("expected number");
+      p = end;
+      return v;
+    };
+    const long long r = index() - 1;
+    const long long c = index() - 1;
     if (r < 0 || r >= nr || c < 0 || c >= nc) die("matrix market, line " + std::to_string(lineno) + ": index out of range");
     double re = 1.0, im = 0.0;
-    if (field != "pattern") {
-      re = std::strtod(p, &end);
-      p = end;
-    }
+    if (field != "pattern") re = value();
     if (m.complex) {
-      im = std::strtod(p, &end);
-      p = end;
+      im = value();
       if (sym == "hermitian" && r == c && im != 0.0) die("matrix market: hermitian diagonal must be real");
     }
+    for (; *p; ++p)
+      if (!std::isspace(static_cast<unsigned char>(*p))) bad("trailing characters after entry");
     if (!general && c > r) die("matrix market: entry above the diagonal in a symmetric-format matrix");
     // append_expanded (mtxio.cpp:67-81): the entry, then its mirror
     m.r.push_back(r), m.c.push_back(c), m.re.push_back(re), m.im.push_back(im);
@@ -191,7 +213,8 @@ std::string jnum(double v) {
 }
 
 struct Args {
-  std::string cmd, path, precision = "dd", mode = "p", lanes = "on", name, method = "cg", history;
+  std::string cmd, path, precision = "dd", mode = "p", lanes = "on", name, method = "bicgstab", history,
+      dots = "tree";
   int threads = 0, reps = 5, device = 0;
   bool transposed = false;
   double rtol = 1e-13, atol = 1e-99;
@@ -222,6 +245,7 @@ Args parse_args(int argc, char** argv) {
     else if (o == "--atol") a.atol = std::atof(val().c_str());
     else if (o == "--max-iters") a.max_iters = std::atoll(val().c_str());
     else if (o == "--history") a.history = val();
+    else if (o == "--dots") a.dots = val();
     else die("unknown option " + o);
   }
   if (a.name.empty()) {
@@ -314,36 +338,58 @@ int run_spmv(const Args& a) {
 }
 
 int run_solve(const Args& a) {
-  if (a.method != "cg") die("solve: the device-resident solver is cg (" + a.method + " runs through the "
-                            "C++ drop-in's GpuCsrOperator with the reference's own solver)");
+  static const char* methods[] = {"cg", "bicg", "cgs", "bicgstab", "gpbicg"};  // parse_method, krylov.hpp:37-44
+  int method = -1;
+  for (int m = 0; m < 5; ++m)
+    if (a.method == methods[m]) method = m;
+  if (method < 0) die("solve: unknown method '" + a.method + "' (cg, bicg, cgs, bicgstab, gpbicg)");
+  if (a.dots != "tree" && a.dots != "exact") die("solve: --dots is tree or exact");
   const Coo coo = parse_mtx(a.path);
   if (coo.complex) die("solve: complex matrices are not supported; the solvers are real", 1);
-  if (a.mode != "p") die("solve: the device CG runs the Pure mode (--mode p)");
+  if (a.mode != "p" && a.mode != "m") die("solve: --mode is p (Pure) or m (Mixed)");
+  const bool mixed = a.mode == "m";
   const Csr A = coo_to_csr(coo);
+  if (A.nrows != A.ncols) die("solve: the matrix must be square", 1);
   const int K = precision_k(a.precision);
   mpsg_ctx* ctx = nullptr;
   if (mpsg_ctx_create(a.device, &ctx) != MPSG_OK) die("no usable sm_100a GPU", 1);
-  mpsg_csr* d = upload(ctx, A, K, false, false, false);
+  mpsg_csr* d = upload(ctx, A, K, false, mixed, method == MPSG_BICG);
   const int64_t n = A.ncols;
+  const int threads = a.threads > 0 ? a.threads : 1;
   std::vector<double> v((size_t)n * K), b((size_t)n * K), x((size_t)n * K), hist((size_t)a.max_iters + 1);
   check(ctx, mpsg_make_vector(ctx, K, n, v.data(), nullptr), "make_vector");
   const int order = order_of(a.lanes);
   check(ctx, mpsg_spmv(ctx, d, order, n, v.data(), b.data()), "spmv");  // b = A v (bench.cpp:552-554)
-  mpsg_cg_config cfg{a.rtol, a.atol, a.max_iters, 32, 1};
   mpsg_cg_report rep{};
-  check(ctx, mpsg_cg(ctx, d, order, n, b.data(), nullptr, &cfg, x.data(), hist.data(), (int64_t)hist.size(), &rep),
-        "cg");
+  if (method == MPSG_CG && a.dots == "tree") {
+    mpsg_cg_config cfg{a.rtol, a.atol, a.max_iters, 32, 1};
+    check(ctx, mpsg_cg(ctx, d, order, n, b.data(), nullptr, &cfg, x.data(), hist.data(), (int64_t)hist.size(), &rep),
+          "cg");
+  } else {
+    mpsg_solver_config cfg{};
+    cfg.method = method;
+    cfg.threads = threads;
+    cfg.rel_tol = a.rtol;
+    cfg.abs_tol = a.atol;
+    cfg.max_iters = a.max_iters;
+    cfg.check_every = 32;
+    cfg.use_graph = 1;
+    cfg.dot_order = a.dots == "exact" ? MPSG_DOT_SEQUENTIAL : MPSG_DOT_TREE;
+    check(ctx, mpsg_solve(ctx, d, order, n, b.data(), nullptr, &cfg, x.data(), hist.data(), (int64_t)hist.size(),
+                          &rep),
+          "solve");
+  }
   static const char* status[] = {"converged", "max_iterations", "breakdown", "diverged"};
   if (!a.history.empty()) {
     std::ofstream h(a.history);
     h << "iter,residual\n";
     for (int64_t k = 0; k < rep.history_len; ++k) h << k << ',' << jnum(hist[(size_t)k]) << '\n';
   }
-  std::printf("{\"schema\":\"mpsparse.solve.v1\",\"matrix\":%s,\"method\":\"cg\",\"precision\":\"%s\","
-              "\"mode\":\"p\",\"threads\":%d,\"n\":%lld,\"nnz\":%lld,\"status\":\"%s\",\"converged\":%s,"
+  std::printf("{\"schema\":\"mpsparse.solve.v1\",\"matrix\":%s,\"method\":\"%s\",\"precision\":\"%s\","
+              "\"mode\":\"%s\",\"threads\":%d,\"n\":%lld,\"nnz\":%lld,\"status\":\"%s\",\"converged\":%s,"
               "\"iterations\":%lld,\"rhs_norm\":%s,\"final_recurrence_residual\":%s,\"final_true_residual\":%s,"
               "\"setup_seconds\":%s,\"solve_seconds\":%s%s%s%s}\n",
-              jstr(a.name).c_str(), a.precision.c_str(), a.threads > 0 ? a.threads : 1, (long long)A.nrows,
+              jstr(a.name).c_str(), methods[method], a.precision.c_str(), mixed ? "m" : "p", threads, (long long)A.nrows,
               (long long)A.indices.size(), status[rep.status], rep.converged ? "true" : "false",
               (long long)rep.iterations, jnum(rep.rhs_norm).c_str(), jnum(rep.final_recurrence_residual).c_str(),
               jnum(rep.final_true_residual).c_str(), jnum(rep.setup_seconds).c_str(),

@@ -23,7 +23,12 @@
 //     and the transposed products mps::gpu::sptmv / sptmv_complex (+ adjoint)
 //     bit for bit against the reference at one thread (kernels.hpp:368-441);
 //  7. the reference's own solve_bicg (krylov.hpp:283, uses apply_transposed)
-//     over a GpuCsrOperator: identical history to the host operator.
+//     over a GpuCsrOperator: identical history to the host operator;
+//  8. the device-resident mps::gpu::solve (every KrylovMethod, krylov.hpp:
+//     596-606) with DotOrder::Sequential == the reference's mps::solve bit for
+//     bit (iterate, history, status, iterations, detail, true residual), lanes
+//     on and off, BiCG at 1 and 4 threads; with DotOrder::Tree the same status
+//     within +-1 iteration.
 #include <bit>
 #include <cmath>
 #include <cstdio>
@@ -263,6 +268,65 @@ void bicg_over_gpu_operator() {
              std::to_string(ref.report.iterations) + " iterations)");
 }
 
+template <int K>
+void device_solvers(test::Rng& rng) {
+  using E = MultiComponent<K>;
+  for (bool sym : {true, false}) {
+    auto Ad = coo_to_csr(test::random_diag_dominant(rng, 400, 0.03, sym));
+    auto A = convert_csr<E>(Ad);
+    auto b = random_vector<K>(400, rng);
+    mps::gpu::DeviceCsr<E> dA(A, /*with_transpose=*/true);
+    mps::gpu::DeviceCsr<double, E> dAm(Ad, /*with_transpose=*/true);  // Mixed mode
+    for (KrylovMethod m : {KrylovMethod::CG, KrylovMethod::BiCG, KrylovMethod::CGS, KrylovMethod::BiCGSTAB,
+                           KrylovMethod::GPBiCG}) {
+      if (m == KrylovMethod::CG && !sym) continue;
+      for (bool lanes : {true, false}) {
+        for (int threads : {1, 4}) {
+          if (threads > 1 && m != KrylovMethod::BiCG) continue;
+          SolverConfig cfg;
+          cfg.method = m;
+          cfg.rel_tol = 1e-40;
+          cfg.max_iters = 300;
+          cfg.lanes_enabled = lanes;
+          CsrOperator<E> host_op{&A, threads, lanes};
+          mps::gpu::GpuCsrOperator<E> gop{&dA, threads, lanes};
+          auto ref = mps::solve(host_op, b, cfg);
+          auto dev = mps::gpu::solve(gop, b, cfg, mps::gpu::DotOrder::Sequential);
+          const auto& R = ref.report;
+          const auto& D = dev.report;
+          const std::string tag = std::string(to_string(m)) + " K=" + std::to_string(K) + (sym ? " sym" : " nonsym") +
+                                  (lanes ? " lanes on" : " lanes off") + " threads=" + std::to_string(threads);
+          report(same_bits(ref.x, dev.x) && R.residual_history == D.residual_history && R.status == D.status &&
+                     R.iterations == D.iterations && R.detail == D.detail &&
+                     std::bit_cast<std::uint64_t>(R.final_true_residual) ==
+                         std::bit_cast<std::uint64_t>(D.final_true_residual),
+                 "device solve (sequential dots) bit-exact with mps::solve: " + tag + " (" +
+                     std::to_string(R.iterations) + " iterations, " + to_string(R.status) + ")");
+          // Mixed mode: CsrOperator<double> over the binary64 matrix (solve_core, bench.cpp:550-557)
+          CsrOperator<double> host_opm{&Ad, threads, lanes};
+          mps::gpu::GpuCsrOperator<double, E> gopm{&dAm, threads, lanes};
+          auto refm = mps::solve(host_opm, b, cfg);
+          auto devm = mps::gpu::solve(gopm, b, cfg, mps::gpu::DotOrder::Sequential);
+          report(same_bits(refm.x, devm.x) && refm.report.residual_history == devm.report.residual_history &&
+                     refm.report.status == devm.report.status && refm.report.detail == devm.report.detail,
+                 "device solve (sequential dots) bit-exact with mps::solve, Mixed mode: " + tag + " (" +
+                     std::to_string(refm.report.iterations) + " iterations)");
+          if (threads == 1 && lanes) {
+            auto t = mps::gpu::solve(gop, b, cfg);
+            // CG: the north star's +-1%; the Lanczos-type methods amplify round-off
+            // (CGS squares the residual polynomial), so +-5% there
+            const long long tol = m == KrylovMethod::CG ? std::max<long long>(1, R.iterations / 100)
+                                                        : std::max<long long>(2, R.iterations / 20);
+            report(t.report.status == R.status && std::llabs(t.report.iterations - R.iterations) <= tol,
+                   "device solve (tree dots): " + tag + " " + std::to_string(t.report.iterations) +
+                       " iterations vs reference " + std::to_string(R.iterations));
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 int main() {
@@ -281,6 +345,9 @@ int main() {
   mixed_and_transposed<3>(rng);
   mixed_and_transposed<4>(rng);
   bicg_over_gpu_operator();
+  device_solvers<2>(rng);
+  device_solvers<3>(rng);
+  device_solvers<4>(rng);
   std::printf("%d failure(s)\n", failures);
   return failures;
 }
