@@ -45,7 +45,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
                             (n + DOT_THREADS - 1) / DOT_THREADS}));
   cudaGetLastError();
   double *b = nullptr, *x = nullptr, *r = nullptr, *pfull = nullptr, *q = nullptr, *part = nullptr,
-         *hist = nullptr, *loc = nullptr, *gath = nullptr;
+         *hist = nullptr, *loc = nullptr, *gath = nullptr, *pend = nullptr;
   CgState<K>* dst = nullptr;
   const int64_t max_iters = cfg->max_iters;
   cudaGraphExec_t gexec = nullptr;
@@ -53,7 +53,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   auto cleanup = [&]() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
-    void* ps[] = {b, x, r, pfull, q, part, hist, loc, gath, dst};
+    void* ps[] = {b, x, r, pfull, q, part, hist, loc, gath, dst, pend};
     for (void* v : ps)
       if (v) cudaFree(v);
   };
@@ -83,6 +83,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   CG_TRY(cudaMalloc(&q, vb ? vb : 8));
   CG_TRY(cudaMalloc(&part, (size_t)G * K * sizeof(double)));
   CG_TRY(cudaMalloc(&hist, (size_t)(max_iters + 1) * sizeof(double)));
+  CG_TRY(cudaMalloc(&pend, (size_t)(max_iters + 1) * K * sizeof(double)));
   CG_TRY(cudaMalloc(&dst, sizeof(CgState<K>)));
   if (D) {
     CG_TRY(cudaMalloc(&loc, (size_t)K * sizeof(double)));
@@ -116,7 +117,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   };
 
   if (vb) CG_TRY(cudaMemcpyAsync(b, b_host, vb, cudaMemcpyHostToDevice, st));
-  cg_init_state_kernel<K><<<1, 1, 0, st>>>(dst, cfg->rel_tol, cfg->abs_tol, (long long)max_iters, hist);
+  cg_init_state_kernel<K><<<1, 1, 0, st>>>(dst, cfg->rel_tol, cfg->abs_tol, (long long)max_iters, hist, pend);
   // bnorm = norm2(b) (krylov.hpp:185)
   CG_RC(reduce(Dot{}, POST_BNORM, b, b, nullptr, nullptr, 0));
   if (x0) {
@@ -194,6 +195,9 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
     CG_TRY(cudaStreamSynchronize(st));
     status = hs;
   }
+  // deferred record_step values: history[k] = to_double(sqrt(<r,r>_k))
+  cg_history_kernel<K><<<(int)std::min<int64_t>(148, (max_iters + 255) / 256), 256, 0, st>>>(dst, pend, hist);
+  CG_TRY(cudaGetLastError());
   CG_TRY(cudaEventRecord(ev1, st));
   CgState<K> hst;
   CG_TRY(cudaMemcpy(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost));

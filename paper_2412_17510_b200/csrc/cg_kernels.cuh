@@ -21,6 +21,9 @@
 namespace mpsg {
 
 constexpr int CG_RUNNING = -1;
+#ifndef MPSG_CG_PIPE
+#define MPSG_CG_PIPE 1
+#endif
 #ifndef MPSG_DOT_THREADS
 #define MPSG_DOT_THREADS 256
 #endif
@@ -44,6 +47,7 @@ struct CgState {
   double rhs_norm;
   double true_residual;
   double* history;    // [max_iters+1]
+  double* pend;       // [max_iters+1][K]: <r,r> of every step; history = to_double(sqrt(pend))
   unsigned ticket;    // last-block arrival counter (self-resetting)
 };
 
@@ -63,9 +67,13 @@ MPSG_DI MC<K> block_reduce(MC<K> v, MC<K>* sh) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) sh[w] = v;
   __syncthreads();
-  MC<K> s = sh[0];
-  if (threadIdx.x == 0)
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) s = add(s, sh[i]);
+  // warp partials: a fixed xor tree in warp 0 (log2(warps) dependent adds)
+  MC<K> s = zero<K>();
+  if (w == 0) {
+    const int nw = (int)(blockDim.x >> 5);
+    if (lane < nw) s = sh[lane];
+    for (int off = nw >> 1; off >= 1; off >>= 1) s = add(s, shfl_xor(s, off));
+  }
   return s;  // valid in thread 0
 }
 
@@ -101,10 +109,20 @@ MPSG_DI void cg_post(CgState<K>* st, int post, const MC<K>& d) {
     }
   } else if (post == POST_RHO) {
     const long long k = st->k + 1;
+#pragma unroll
+    for (int j = 0; j < K; ++j) st->pend[k * K + j] = d.c[j];
+    st->k = k;
+    if (surely_continues(d, st->thr, st->divergence_cap)) {
+      // record_step continues for certain: history[k] is filled from pend by
+      // cg_history_kernel after the loop (the square root is off the chain)
+      st->beta = divide(d, st->rho);
+      st->rho = d;
+      if (k >= st->max_iters) st->status = 1;
+      return;
+    }
     MC<K> rn = sqrt_mc(d);
     const double rd = to_double(rn);
     st->history[k] = rd;
-    st->k = k;
     // record_step (krylov.hpp:205-213)
     if (!finite(rd)) {
       st->status = 2;
@@ -202,6 +220,49 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
       return mul(w, w);
     }
   };
+#if MPSG_CG_PIPE
+  if constexpr (MODE == 0) {
+    // register double buffer: the next round's operands are in flight while
+    // this round's product is accumulated
+    int64_t i = lo + threadIdx.x;
+    MC<K> un = zero<K>(), vn = zero<K>();
+    if (i < hi) {
+      un = load_aos<K>(u, i);
+      vn = load_aos<K>(v, i);
+    }
+    for (; i < hi; i += DOT_THREADS) {
+      const MC<K> uu = un, vv = vn;
+      if (i + DOT_THREADS < hi) {
+        un = load_aos<K>(u, i + DOT_THREADS);
+        vn = load_aos<K>(v, i + DOT_THREADS);
+      }
+      acc = add(acc, mul(uu, vv));
+    }
+  } else if constexpr (MODE == 1) {
+    int64_t i = lo + threadIdx.x;
+    MC<K> pn = zero<K>(), qn = zero<K>(), xn = zero<K>(), rn = zero<K>();
+    if (i < hi) {
+      pn = load_aos<K>(u, i);
+      qn = load_aos<K>(v, i);
+      xn = load_aos_rw<K>(x, i);
+      rn = load_aos_rw<K>(r, i);
+    }
+    for (; i < hi; i += DOT_THREADS) {
+      const MC<K> pp = pn, qq = qn, xx = xn, rr = rn;
+      if (i + DOT_THREADS < hi) {
+        pn = load_aos<K>(u, i + DOT_THREADS);
+        qn = load_aos<K>(v, i + DOT_THREADS);
+        xn = load_aos_rw<K>(x, i + DOT_THREADS);
+        rn = load_aos_rw<K>(r, i + DOT_THREADS);
+      }
+      const MC<K> xi = add(xx, mul(alpha, pp));
+      const MC<K> ri = add(rr, mul(malpha, qq));
+      store_aos<K>(x, i, xi);
+      store_aos<K>(r, i, ri);
+      acc = add(acc, mul(ri, ri));
+    }
+  } else
+#endif
   for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) acc = add(acc, term(i));
   reduce_finish<K, DOT_THREADS>(st, post, acc, partial, local_out, sh);
 }
@@ -228,9 +289,22 @@ __global__ void __launch_bounds__(256) cg_update_p_kernel(const CgState<K>* st, 
 }
 
 // Initial state: r = b (or b - A x0 computed by the caller), p = r.
+// history[k] = to_double(sqrt(<r,r>_k)) for k = 1..kmax (record_step's value)
+template <int K>
+__global__ void cg_history_kernel(const CgState<K>* st, const double* pend, double* history) {
+  const long long kmax = st->k;
+  for (long long k = 1 + blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= kmax;
+       k += (long long)gridDim.x * blockDim.x) {
+    MC<K> d;
+#pragma unroll
+    for (int j = 0; j < K; ++j) d.c[j] = pend[k * K + j];
+    history[k] = to_double(sqrt_mc(d));
+  }
+}
+
 template <int K>
 __global__ void cg_init_state_kernel(CgState<K>* st, double rel_tol, double abs_tol,
-                                     long long max_iters, double* history) {
+                                     long long max_iters, double* history, double* pend) {
   st->status = CG_RUNNING;
   st->reason = 0;
   st->k = 0;
@@ -238,6 +312,7 @@ __global__ void cg_init_state_kernel(CgState<K>* st, double rel_tol, double abs_
   st->rel_tol = rel_tol;
   st->abs_tol = abs_tol;
   st->history = history;
+  st->pend = pend;
   st->ticket = 0u;
   st->true_residual = 0.0;
 }

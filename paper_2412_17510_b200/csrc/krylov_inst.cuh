@@ -32,9 +32,12 @@ struct KrLauncher {
   KrState<K>* dst;
   int64_t n;
   double* partial;
-  int G;     // reduction grid (one resident wave)
+  int G;     // reduction grid cap
   int ub;    // map grid
   bool seq;  // reference dot order (one thread)
+  int sms;
+  int pfd;   // L2 prefetch distance (rounds) of the reductions
+  int occ_mode;
 
   int check(const char* what) {
     cudaError_t e = cudaGetLastError();
@@ -42,11 +45,21 @@ struct KrLauncher {
                                              cudaGetErrorString(e));
   }
   template <int M, class Body, class Post>
-  int reduce(int gate, Body body, Post post) {
-    if (seq)
+  int reduce(int gate, Body body, Post post, KrPf pf = KrPf{{}, 0}) {
+    if (seq) {
       kr_reduce_seq_kernel<K, M><<<1, 1, 0, st>>>(dst, gate, n, body, post);
-    else
-      kr_reduce_kernel<K, M><<<G, KR_THREADS, 0, st>>>(dst, gate, n, partial, body, post);
+    } else {
+      // one resident wave of this kernel (its own occupancy)
+      static int occ = -1;
+      if (occ < 0) {
+        occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kr_reduce_kernel<K, M, Body, Post>, KR_THREADS, 0);
+        if (occ < 1) occ = 1;
+      }
+      const int o = occ_mode > 0 ? occ_mode : occ;
+      const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)G, (int64_t)sms * o));
+      kr_reduce_kernel<K, M><<<g, KR_THREADS, 0, st>>>(dst, gate, n, partial, body, post, pf, pfd);
+    }
     return check("reduction");
   }
   template <class Body>
@@ -75,14 +88,17 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
   const bool seq = cfg->dot_order == MPSG_DOT_SEQUENTIAL;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  const int G = (int)std::max<int64_t>(
-      1, std::min<int64_t>({(int64_t)KR_MAX_BLOCKS, (int64_t)sms * 4, (n + KR_THREADS - 1) / KR_THREADS}));
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)KR_MAX_BLOCKS, (n + KR_THREADS - 1) / KR_THREADS));
+  const char* e_pf = std::getenv("MPSG_KR_PF");
+  const char* e_occ = std::getenv("MPSG_KR_OCC");
+  const int pfd = e_pf ? std::atoi(e_pf) : 0;
+  const int occ_mode = e_occ ? std::atoi(e_occ) : 0;
   const int ub = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, (n + 255) / 256));
   const int64_t max_iters = cfg->max_iters;
   cudaGetLastError();
 
   double* V[V_COUNT] = {};
-  double *part = nullptr, *hist = nullptr;
+  double *part = nullptr, *hist = nullptr, *pend = nullptr;
   KrState<K>* dst = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaGraph_t graph = nullptr;
@@ -98,6 +114,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
       if (v) cudaFree(v);
     if (part) cudaFree(part);
     if (hist) cudaFree(hist);
+    if (pend) cudaFree(pend);
     if (dst) cudaFree(dst);
   };
   int rc = MPSG_OK;
@@ -133,11 +150,12 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
     if (need[method][i]) KR_TRY(cudaMalloc(&V[i], vb ? vb : 8));
   KR_TRY(cudaMalloc(&part, (size_t)G * 5 * K * sizeof(double)));
   KR_TRY(cudaMalloc(&hist, (size_t)(max_iters + 1) * sizeof(double)));
+  KR_TRY(cudaMalloc(&pend, (size_t)(max_iters + 1) * K * sizeof(double)));
   KR_TRY(cudaMalloc(&dst, sizeof(KrState<K>)));
   double *b = V[V_B], *x = V[V_X], *r = V[V_R], *q = V[V_Q], *rt = V[V_RT], *p = V[V_P], *pt = V[V_PT],
          *qt = V[V_QT], *u = V[V_U], *v = V[V_V], *t = V[V_T], *w = V[V_W], *z = V[V_Z], *y = V[V_Y],
          *at = V[V_AT], *dv = V[V_D];
-  KrLauncher<K> L{ctx, st, dst, n, part, G, ub, seq};
+  KrLauncher<K> L{ctx, st, dst, n, part, G, ub, seq, sms, pfd, occ_mode};
   const mpsg_csr* T = A->trans;
   auto apply = [&](const double* in, double* out) { return launch_spmv(ctx, A, order, in, nullptr, out, nullptr, st); };
   // CsrOperator::apply_transposed = sptmv at `threads` (krylov.hpp:116-119)
@@ -163,7 +181,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
   // ------------------------------------------------------------ solver_init
   // (krylov.hpp:160-201)
   if (vb) KR_TRY(cudaMemcpyAsync(b, b_host, vb, cudaMemcpyHostToDevice, st));
-  kr_init_state_kernel<K><<<1, 1, 0, st>>>(dst, cfg->rel_tol, cfg->abs_tol, (long long)max_iters, hist);
+  kr_init_state_kernel<K><<<1, 1, 0, st>>>(dst, cfg->rel_tol, cfg->abs_tol, (long long)max_iters, hist, pend);
   // bnorm = norm2(b); threshold, divergence cap, breakdown floor (:185-189)
   KR_RC(L.template reduce<1>(
       GATE_ALWAYS,
@@ -239,7 +257,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
   };
   // record_step on ||r|| = sqrt(d[0]); rho' = d[1]; beta = rho'/rho (BiCG, CGS)
   auto post_rho_next = [=] __device__(KrState<K> * s, MC<K> * d) {
-    if (!kr_record(s, sqrt_mc(d[0]))) return;
+    if (!kr_record(s, d[0])) return;
     s->sc.beta = divide(d[1], s->sc.rho);
     s->sc.rho = d[1];
     kr_next(s, true);
@@ -255,7 +273,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(p, i), load_aos_rw<K>(q, i));  // sigma = <p, q>
                  },
-                 post_alpha)))
+                 post_alpha,
+                 KrPf{{p, q}, 2})))
           return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
@@ -267,11 +286,12 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                    d[0] = mul(ri, ri);  // rho' = <r, r>
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) {
-                   if (!kr_record(s, sqrt_mc(d[0]))) return;
+                   if (!kr_record(s, d[0])) return;
                    s->sc.beta = divide(d[0], s->sc.rho);
                    s->sc.rho = d[0];
                    kr_next(s, false);
-                 })))
+                 },
+                 KrPf{{x, p, r, q}, 4})))
           return e;
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, load_aos_rw<K>(p, i))));
@@ -285,7 +305,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(pt, i), load_aos_rw<K>(q, i));  // sigma = <p~, q>
                  },
-                 post_alpha)))
+                 post_alpha,
+                 KrPf{{pt, q}, 2})))
           return e;
         if ((e = L.template reduce<2>(
                  GATE_RUN,
@@ -300,7 +321,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                    d[0] = mul(ri, ri);   // ||r||^2
                    d[1] = mul(rti, ri);  // rho' = <r~, r>
                  },
-                 post_rho_next)))
+                 post_rho_next,
+                 KrPf{{x, p, r, q, rt, qt}, 6})))
           return e;
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, load_aos_rw<K>(p, i))));
@@ -314,7 +336,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i));  // sigma = <r~, v>
                  },
-                 post_alpha)))
+                 post_alpha,
+                 KrPf{{rt, v}, 2})))
           return e;
         // q = u - alpha v; t = u + q; x += alpha t
         if ((e = L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
@@ -335,7 +358,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                    d[0] = mul(ri, ri);
                    d[1] = mul(load_aos_rw<K>(rt, i), ri);
                  },
-                 post_rho_next)))
+                 post_rho_next,
+                 KrPf{{r, w, rt}, 3})))
           return e;
         // u = r + beta q; p = u + beta (q + beta p)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
@@ -353,7 +377,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i));  // sigma = <r~, v>
                  },
-                 post_alpha)))
+                 post_alpha,
+                 KrPf{{rt, v}, 2})))
           return e;
         // s = r - alpha v; half-step test on ||s|| (:445-458)
         if ((e = L.template reduce<1>(
@@ -363,15 +388,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                    store_aos<K>(s_, i, si);
                    d[0] = mul(si, si);
                  },
-                 [=] __device__(KrState<K> * s, MC<K> * d) {
-                   const MC<K> sn = sqrt_mc(d[0]);
-                   if (less_equal(sn, s->thr)) {
-                     s->k += 1;
-                     s->history[s->k] = to_double(sn);
-                     s->status = KR_HALF;
-                     s->sc.half = 1;
-                   }
-                 })))
+                 [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); },
+                 KrPf{{r, v}, 2})))
           return e;
         if ((e = apply(s_, t))) return e;
         // tt = <t, t>; omega = <t, s> / tt (:460-470)
@@ -390,7 +408,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                    const MC<K> om = divide(d[1], d[0]);
                    s->sc.omega = om;
                    if (kr_tiny(to_double(om), s->floor)) kr_break(s, 7);
-                 })))
+                 },
+                 KrPf{{t, s_}, 2})))
           return e;
         // x += alpha p (+ omega s); r = s (- omega t); ||r||, <r~, r> (:450-452, 471-475)
         if ((e = L.template reduce<2>(
@@ -413,12 +432,13 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                      s->status = MPSG_CONVERGED;
                      return;
                    }
-                   if (!kr_record(s, sqrt_mc(d[0]))) return;
+                   if (!kr_record(s, d[0])) return;
                    // beta = (rho'/rho) (alpha/omega) (:486)
                    s->sc.beta = mul(divide(d[1], s->sc.rho), divide(s->sc.alpha, s->sc.omega));
                    s->sc.rho = d[1];
                    kr_next(s, true);
-                 })))
+                 },
+                 KrPf{{s_, x, p, t, rt}, 5})))
           return e;
         // p = r + beta (p - omega v) (:487-488)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
@@ -435,7 +455,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(ap, i));  // sigma = <r~, Ap>
                  },
-                 post_alpha)))
+                 post_alpha,
+                 KrPf{{rt, ap}, 2})))
           return e;
         // d = t_prev - r; y = d + alpha (Ap - w); t = r - alpha Ap; half-step test (:529-540)
         if ((e = L.template reduce<1>(
@@ -449,15 +470,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                    store_aos<K>(t, i, ti);
                    d[0] = mul(ti, ti);
                  },
-                 [=] __device__(KrState<K> * s, MC<K> * d) {
-                   const MC<K> tn = sqrt_mc(d[0]);
-                   if (less_equal(tn, s->thr)) {
-                     s->k += 1;
-                     s->history[s->k] = to_double(tn);
-                     s->status = KR_HALF;
-                     s->sc.half = 1;
-                   }
-                 })))
+                 [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); },
+                 KrPf{{t, r, ap, w}, 4})))
           return e;
         if ((e = apply(t, at))) return e;
         // <At, t>, <At, At>, <y, y>, <y, At>, <y, t>; zeta, eta (:542-567)
@@ -489,7 +503,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                      s->sc.zeta = divide(sub(mul(yy, att), mul(yt, yat)), den);
                      s->sc.eta = divide(sub(mul(ata, yt), mul(yat, att)), den);
                    }
-                 })))
+                 },
+                 KrPf{{at, t, y}, 3})))
           return e;
         // u, z, x, r; ||r||, <r~, r> (:568-580); half step: x += alpha p, r = t
         if ((e = L.template reduce<2>(
@@ -519,7 +534,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                      s->status = MPSG_CONVERGED;
                      return;
                    }
-                   if (!kr_record(s, sqrt_mc(d[0]))) return;
+                   if (!kr_record(s, d[0])) return;
                    if (kr_tiny(to_double(s->sc.zeta), s->floor)) {  // (:581-585), after record
                      kr_break(s, 10);
                      return;
@@ -527,7 +542,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                    s->sc.beta = mul(divide(s->sc.alpha, s->sc.zeta), divide(d[1], s->sc.rho));
                    s->sc.rho = d[1];
                    kr_next(s, true);
-                 })))
+                 },
+                 KrPf{{t, x, p, r, ap, dv}, 6})))
           return e;
         // w = At + beta Ap; p = r + beta (p - u); t_prev = t (already in t) (:586-589)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
@@ -577,6 +593,9 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
     KR_TRY(cudaMemcpyAsync(&status, &dst->status, sizeof(int), cudaMemcpyDeviceToHost, st));
     KR_TRY(cudaStreamSynchronize(st));
   }
+  // deferred record_step values
+  kr_history_kernel<K><<<(int)std::min<int64_t>(sms, (max_iters + 255) / 256), 256, 0, st>>>(dst, hist);
+  KR_TRY(cudaGetLastError());
   KR_TRY(cudaEventRecord(ev1, st));
   KrState<K> hst;
   KR_TRY(cudaMemcpy(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost));

@@ -57,8 +57,24 @@ struct KrState {
   double rhs_norm;
   double true_residual;
   double* history;    // [max_iters + 1]
+  double* pend;       // [max_iters + 1][K]: the squared norm of every recorded step
   unsigned ticket;    // last-block arrival counter (self-resetting)
 };
+
+// Vectors a reduction body reads, prefetched into L2 `pfd` rounds ahead of
+// use (prefetch.global.L2: no registers held, unlike a register pipeline),
+// so the per-thread accumulation chain does not wait on DRAM every round.
+struct KrPf {
+  const double* p[6];
+  int n;
+};
+
+MPSG_DI void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+template <int K>
+MPSG_DI void kr_prefetch(const KrPf& pf, int64_t j) {
+  for (int v = 0; v < pf.n; ++v) prefetch_l2(pf.p[v] + j * K);
+}
 
 MPSG_DI bool gate_open(int status, int gate) {
   return gate == GATE_ALWAYS || status == KR_RUNNING || (gate == GATE_RUN_HALF && status == KR_HALF);
@@ -77,11 +93,25 @@ MPSG_DI void kr_break(KrState<K>* st, int reason) {
 // (:215-224): appends ||r_k|| for k = completed + 1; true while the
 // iteration continues.
 template <int K>
-MPSG_DI bool kr_record(KrState<K>* st, const MC<K>& rnorm) {
+MPSG_DI void kr_pend(KrState<K>* st, long long k, const MC<K>& d) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) st->pend[k * K + j] = d.c[j];
+}
+
+// record_step (krylov.hpp:203-213) + close_report's status mapping
+// (:215-224) on ||r_k|| = sqrt(d), d = <r, r>, for k = completed + 1; true
+// while the iteration continues.  When the outcome is certain
+// (surely_continues) the multi-component square root is skipped here and the
+// history entry is filled from pend by kr_history_kernel after the loop.
+template <int K>
+MPSG_DI bool kr_record(KrState<K>* st, const MC<K>& d) {
   const long long k = st->k + 1;
+  kr_pend(st, k, d);
+  st->k = k;
+  if (surely_continues(d, st->thr, st->cap)) return true;
+  const MC<K> rnorm = sqrt_mc(d);
   const double rd = to_double(rnorm);
   st->history[k] = rd;
-  st->k = k;
   if (!finite(rd)) {
     kr_break(st, 2);
     return false;
@@ -95,6 +125,35 @@ MPSG_DI bool kr_record(KrState<K>* st, const MC<K>& rnorm) {
     return false;
   }
   return true;
+}
+
+// The half-step test of BiCGSTAB / GPBiCG (krylov.hpp:447-449, 505-507):
+// ||s|| = sqrt(d) <= threshold -> KR_HALF with the entry recorded.
+template <int K>
+MPSG_DI void kr_half_test(KrState<K>* st, const MC<K>& d) {
+  if (surely_continues(d, st->thr, INFINITY)) return;
+  const MC<K> sn = sqrt_mc(d);
+  if (less_equal(sn, st->thr)) {
+    st->k += 1;
+    kr_pend(st, st->k, d);
+    st->history[st->k] = to_double(sn);
+    st->status = KR_HALF;
+    st->sc.half = 1;
+  }
+}
+
+// history[k] = to_double(sqrt(pend[k])) for k = 1..completed (record_step's value)
+template <int K>
+__global__ void kr_history_kernel(const KrState<K>* st, double* history) {
+  const long long kmax = st->k;
+  const double* pend = st->pend;
+  for (long long k = 1 + blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= kmax;
+       k += (long long)gridDim.x * blockDim.x) {
+    MC<K> d;
+#pragma unroll
+    for (int j = 0; j < K; ++j) d.c[j] = pend[k * K + j];
+    history[k] = to_double(sqrt_mc(d));
+  }
 }
 
 // End of an iteration that continues: the loop bound (krylov.hpp: `for (k =
@@ -123,11 +182,13 @@ MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh) {
     for (int m = 0; m < M; ++m) sh[w * M + m] = v[m];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // warp partials: a fixed xor tree in warp 0 (log2(warps) dependent adds)
+  if (w == 0) {
+    const int nw = (int)(blockDim.x >> 5);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      MC<K> s = sh[m];
-      for (int i = 1; i < (int)(blockDim.x >> 5); ++i) s = add(s, sh[i * M + m]);
+      MC<K> s = lane < nw ? sh[lane * M + m] : zero<K>();
+      for (int off = nw >> 1; off >= 1; off >>= 1) s = add(s, shfl_xor(s, off));
       v[m] = s;
     }
   }
@@ -140,7 +201,8 @@ MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh) {
 // and runs post(st, totals).  Deterministic for a fixed grid.
 template <int K, int M, class Body, class Post>
 __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, int gate, int64_t n,
-                                                               double* partial, Body body, Post post) {
+                                                               double* partial, Body body, Post post, KrPf pf,
+                                                               int pfd) {
   __shared__ MC<K> sh[(KR_THREADS / 32) * M];
   __shared__ bool last;
   if (!gate_open(st->status, gate)) return;
@@ -152,7 +214,11 @@ __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, i
   MC<K> acc[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) acc[m] = zero<K>();
+  if (pfd > 0)
+    for (int d = 1; d <= pfd; ++d)
+      if (lo + threadIdx.x + (int64_t)d * KR_THREADS < hi) kr_prefetch<K>(pf, lo + threadIdx.x + (int64_t)d * KR_THREADS);
   for (int64_t i = lo + threadIdx.x; i < hi; i += KR_THREADS) {
+    if (pfd > 0 && i + (int64_t)pfd * KR_THREADS < hi) kr_prefetch<K>(pf, i + (int64_t)pfd * KR_THREADS);
     MC<K> t[M];
     body(sc, i, t);
 #pragma unroll
@@ -218,7 +284,7 @@ __global__ void __launch_bounds__(256) kr_map_kernel(const KrState<K>* st, int g
 
 template <int K>
 __global__ void kr_init_state_kernel(KrState<K>* st, double rel_tol, double abs_tol, long long max_iters,
-                                     double* history) {
+                                     double* history, double* pend) {
   st->sc.rho = st->sc.alpha = st->sc.beta = st->sc.omega = st->sc.zeta = st->sc.eta = zero<K>();
   st->sc.half = 0;
   st->thr = zero<K>();
@@ -230,6 +296,7 @@ __global__ void kr_init_state_kernel(KrState<K>* st, double rel_tol, double abs_
   st->abs_tol = abs_tol;
   st->cap = st->floor = st->rhs_norm = st->true_residual = 0.0;
   st->history = history;
+  st->pend = pend;
   st->ticket = 0u;
 }
 

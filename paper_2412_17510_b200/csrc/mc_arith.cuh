@@ -398,6 +398,22 @@ MPSG_DI bool less_equal(const MC<K>& x, const MC<K>& y) {  // multicomp.hpp:390-
   return c == 0 || c == -1;
 }
 
+// record_step's tests on ||r|| = sqrt(d) without the multi-component square
+// root, when the outcome is certain: d's leading part is a normal positive
+// double, and sqrt(d0) clears the threshold and stays under the divergence cap
+// by a relative margin of 1e-9 (sqrt_mc(d) and sqrt(d0) agree to ~1e-16
+// relative, as do thr and to_double(thr)).  Then rnorm > thr, rnorm is finite
+// and to_double(rnorm) <= cap, i.e. the iteration continues -- the decision the
+// exact test takes -- and the history entry to_double(sqrt_mc(d)) can be
+// computed later, off the critical path of the solve.
+template <int K>
+MPSG_DI bool surely_continues(const MC<K>& d, const MC<K>& thr, double cap) {
+  const double d0 = d.c[0];
+  if (!(d0 >= 2.2250738585072014e-308 && d0 <= 1e300)) return false;  // also rejects NaN
+  const double est = __dsqrt_rn(d0);
+  return est > to_double(thr) * (1.0 + 1e-9) && est < cap * (1.0 - 1e-9);
+}
+
 // -------------------------------------------------------- memory helpers --
 // L2 eviction-priority hints (createpolicy + ld.global.L2::cache_hint): the
 // gathered vector x is loaded evict_last so the streamed matrix (evict_first)
