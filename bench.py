@@ -77,6 +77,25 @@ def cg_iter_ops(nnz, n, K):
     return (nnz + 5 * n) * OPS_PER_NNZ[K]
 
 
+# Per-iteration algorithmic work of the other device solvers (krylov_inst.cuh),
+# as (SpMVs, multi-component mul+add pairs per element, vector passes of n*8K
+# bytes incl. each SpMV's input and output):
+#   BiCGSTAB: <r~,v>; s = r - alpha v, <s,s>; <t,t>, <t,s>; x += alpha p + omega s,
+#   r = s - omega t, <r,r>, <r~,r>; p = r + beta (p - omega v)  -> 2 SpMV, 12 pairs, 22 passes
+SOLVER_WORK = {"bicgstab": (2, 12, 22)}
+SOLVER_ITERS = 200
+
+
+def solver_iter_bytes(method, nnz, n, K):
+    s, _, passes = SOLVER_WORK[method]
+    return s * (nnz * (8 * K + 4) + 4 * (n + 1)) + passes * n * 8 * K
+
+
+def solver_iter_ops(method, nnz, n, K):
+    s, pairs, _ = SOLVER_WORK[method]
+    return (s * nnz + pairs * n) * OPS_PER_NNZ[K]
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -165,7 +184,20 @@ def run_reference(steps, warmup, cfg, K, cg=False, threads=None):
     kind = "reference" if O.ref_available() else "port"
     order = 1  # lanes on: the reference default (kernels.hpp:44)
     nnz = A.nnz
-    if cg:
+    if isinstance(cg, str) and cg != "cg":
+        # a bounded prefix of the solve (serial vector ops, krylov.hpp:122-140)
+        iters = 2
+        if kind == "reference":
+            b = O.ref_spmv(A, x, order, threads=threads)
+            call = lambda: O.ref_solve(A, b, cg, order, threads=threads, rel_tol=1e-99, max_iters=iters)  # noqa
+        else:
+            threads = 1
+            b = O.spmv(A, x, order)
+            call = lambda: O.solve(A, b, cg, order, rel_tol=1e-99, max_iters=iters)  # noqa: E731
+        units = SOLVER_WORK[cg][0] * nnz * iters
+        sample = (f"cfg5 {K_NAME[K]} {cg}, first {iters} of {SOLVER_ITERS} iterations (SpMV on {threads} "
+                  f"OpenMP threads, vector ops serial as in krylov.hpp:122-140)")
+    elif cg:
         # a bounded prefix of the 500-iteration solve (the serial vector ops of
         # krylov.hpp:122-140 dominate; the full run is minutes to tens of minutes)
         iters = 3
@@ -361,8 +393,10 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant="pure"):
     return res
 
 
-def run_gpu_cg(args, K, order, rank, world, dist):
-    """Config 5: 500 CG iterations (fixed budget, rel_tol 1e-30 so none stops early)."""
+def run_gpu_cg(args, K, order, rank, world, dist, method="cg"):
+    """Config 5: 500 CG iterations (fixed budget, rel_tol 1e-30 so none stops early);
+    method != "cg": that device solver (mpsg_solve, tree dots) for up to
+    SOLVER_ITERS iterations, units = SpMVs x nnz x iterations done."""
     import torch
 
     import paper_2412_17510_b200 as M
@@ -371,10 +405,18 @@ def run_gpu_cg(args, K, order, rank, world, dist):
     stream, ctx = setup_stream(torch, M, dev)
     A, xt = make_inputs("cfg5", K)
     n, nnz = A.nrows, A.nnz
-    shard = args.shard and world > 1
-    cfg = M.SolverConfig(rel_tol=1e-30, max_iters=CG_ITERS, lanes_enabled=order != 0, fast=order == 2)
+    shard = args.shard and world > 1 and method == "cg"
+    iters = CG_ITERS if method == "cg" else SOLVER_ITERS
+    cfg = M.SolverConfig(method=M.parse_method(method), rel_tol=1e-30 if method == "cg" else 1e-99,
+                         max_iters=iters, lanes_enabled=order != 0, fast=order == 2)
     comm = None
-    if shard:
+    if method != "cg":
+        dA = M.DeviceCsr(A, K, ctx=ctx)
+        b = M.spmv(dA, xt, M.ORDER_LANE4)
+        op = M.CsrOperator(dA)
+        solve = lambda: M.solve(op, b, cfg)  # noqa: E731
+        units = None
+    elif shard:
         comm = make_comm(M, ctx, world, rank, dist)
         dA = M.DistCsr.from_global(comm, A, K)
         b0, e0 = dA.row_begin, dA.row_end
@@ -407,13 +449,17 @@ def run_gpu_cg(args, K, order, rank, world, dist):
     t_loop = max_over_ranks(torch, dev, dist, statistics.median(loop))
     t_wall = max_over_ranks(torch, dev, dist, statistics.median(wall))
     rep = res.report
-    out = dict(n=n, nnz=nnz, units=units, t_total=t_loop, per_iter=t_loop / CG_ITERS, clocks=clocks,
-               e2e={"value": units / t_wall / 1e9, "unit": "Gnnz/s (CG SpMV work)",
-                    "h2d_bytes_per_step": int(b.nbytes), "d2h_bytes_per_step": int(b.nbytes) + 8 * (CG_ITERS + 1),
-                    "call": "mpsg_dcg" if shard else "mpsg_cg"},
+    if units is None:  # other solvers: the iterations actually run
+        iters = max(rep.iterations, 1)
+        units = world * SOLVER_WORK[method][0] * nnz * iters
+    out = dict(n=n, nnz=nnz, units=units, t_total=t_loop, per_iter=t_loop / iters, clocks=clocks,
+               e2e={"value": units / t_wall / 1e9, "unit": f"Gnnz/s ({method} SpMV work)",
+                    "h2d_bytes_per_step": int(b.nbytes), "d2h_bytes_per_step": int(b.nbytes) + 8 * (iters + 1),
+                    "call": "mpsg_dcg" if shard else ("mpsg_cg" if method == "cg" else "mpsg_solve")},
+               method=method, iters=iters,
                iterations=rep.iterations, rel_residual=rep.residual_history[-1] / rep.residual_history[0],
                true_residual=rep.final_true_residual, shard=shard, cplx=False, halo_rows=0,
-               launches=CG_ITERS * 5)
+               launches=iters * (5 if method == "cg" else 9))
     del dA
     if comm:
         comm.close()
@@ -424,6 +470,8 @@ def run_gpu_cg(args, K, order, rank, world, dist):
 def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey, mixed=False):
     if kind == "cg":
         byts, ops = cg_iter_bytes(nnz, n, K), cg_iter_ops(nnz, n, K)
+    elif kind in SOLVER_WORK:
+        byts, ops = solver_iter_bytes(kind, nnz, n, K), solver_iter_ops(kind, nnz, n, K)
     else:
         byts, ops = algorithmic_bytes(nnz, n, K, cplx, mixed), algorithmic_ops(nnz, K, cplx, mixed)
     t_hbm, t_fp = byts / (hbm_peak * 1e9), ops / fp64_peak
@@ -437,7 +485,7 @@ def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey, mixed=Fa
         roof = {"bound": "fp64", "achieved": ach, "peak": pk, "unit": "T fp64 instr/s", "frac": ach / pk,
                 "peak_source": "measured on this GPU by mpsg_measure_fp64_peak (DFMA throughput)"}
     roof.update(t_roofline_us=max(t_hbm, t_fp) * 1e6, algorithmic_bytes=byts, algorithmic_fp64_ops=ops,
-                per=("one CG iteration" if kind == "cg" else "one SpMV launch"),
+                per=(f"one {kind} iteration" if kind != "spmv" else "one SpMV launch"),
                 traffic=traffic_for(tkey))
     return roof
 
@@ -453,6 +501,7 @@ def main():
     ap.add_argument("--order", default="fast", choices=["fast", "lane4", "scalar"])
     ap.add_argument("--shard", action="store_true", help="row-shard the matrix across ranks (configs 3, 4, 5)")
     ap.add_argument("--cg", action="store_true", help="config 5: 500-iteration CG instead of one SpMV")
+    ap.add_argument("--solver", default="", help="config 5: a device solver (bicgstab) instead of one SpMV")
     ap.add_argument("--variant", default="pure", choices=["pure", "mixed", "sptmv"],
                     help="mixed: binary64 matrix (the paper's M mode); sptmv: y = A^T x")
     ap.add_argument("--all", action="store_true", help="one line per config/precision (not the driver line)")
@@ -461,7 +510,9 @@ def main():
     ap.add_argument("--secondary", default="", help="'none' disables the TD line beside the cfg2 QD headline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    if args.cg:
+    if args.solver == "cg":
+        args.cg, args.solver = True, ""
+    if args.cg or args.solver:
         args.config = "cfg5"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -472,12 +523,13 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        r = run_reference(args.steps, args.warmup, args.config, args.K, cg=args.cg)
+        r = run_reference(args.steps, args.warmup, args.config, args.K, cg=args.solver or args.cg)
         line = {"metric": METRIC, "value": r["value"], "unit": "Gnnz/s", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": r["median_s"] * 1e3, "higher_is_better": True,
                 "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded generators, synth/mpsgen.c)", "impl": "reference",
-                "config": {"workload": f"{args.config} {K_NAME[args.K]}{' CG' if args.cg else ''}: "
+                "config": {"workload": f"{args.config} {K_NAME[args.K]}"
+                                       f"{(' ' + (args.solver or 'cg').upper()) if (args.cg or args.solver) else ''}: "
                                        f"{CONFIG_DESC[args.config]}",
                            "precision": K_NAME[args.K], "order": "lane4 (reference default)"},
                 "cpu_baseline": {"value": r["value"], "unit": "Gnnz/s", "cores": r["cores"], "kind": r["kind"],
@@ -505,13 +557,14 @@ def main():
     fp64_peak = M.measure_fp64_peak(probe)
     probe.close()
 
-    jobs = [(args.config, args.K, args.cg, args.variant)]
+    jobs = [(args.config, args.K, args.solver or args.cg, args.variant)]
     if args.all:
         jobs = [("cfg1", 2, False, "pure"), ("cfg2", 3, False, "pure"), ("cfg2", 4, False, "pure"),
                 ("cfg3", 2, False, "pure"), ("cfg3", 4, False, "pure"), ("cfg4", 2, False, "pure"),
                 ("cfg5", 2, False, "pure"), ("cfg5", 4, False, "pure"), ("cfg5", 2, True, "pure"),
                 ("cfg5", 4, True, "pure"), ("cfg2", 4, False, "mixed"), ("cfg4", 2, False, "mixed"),
-                ("cfg3", 4, False, "mixed"), ("cfg2", 4, False, "sptmv"), ("cfg3", 2, False, "sptmv")]
+                ("cfg3", 4, False, "mixed"), ("cfg2", 4, False, "sptmv"), ("cfg3", 2, False, "sptmv"),
+                ("cfg5", 2, "bicgstab", "pure"), ("cfg5", 4, "bicgstab", "pure")]
     secondary = None
     if (not args.all and args.config == "cfg2" and args.K == 4 and not args.cg and args.variant == "pure"
             and args.secondary != "none"):
@@ -520,10 +573,11 @@ def main():
     results = []
     for cfg, K, cg, variant in jobs + ([secondary] if secondary else []):
         if cg:
-            r = run_gpu_cg(args, K, order, rank, world, dist)
+            meth = cg if isinstance(cg, str) else "cg"
+            r = run_gpu_cg(args, K, order, rank, world, dist, meth)
             r["variant"] = "pure"
-            r["roof"] = roofline("cg", r["nnz"], r["n"], K, False, r["per_iter"], hbm_peak, fp64_peak,
-                                 f"cg5_K{K}")
+            r["roof"] = roofline(meth, r["nnz"], r["n"], K, False, r["per_iter"], hbm_peak, fp64_peak,
+                                 f"cg5_K{K}" if meth == "cg" else f"{meth}5_K{K}")
         else:
             r = run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant)
             tkey = f"{cfg}_K{K}" + ("" if variant == "pure" else f"_{variant}")
@@ -546,14 +600,17 @@ def main():
                     "higher_is_better": True, "scaling": "strong" if r["shard"] else "weak",
                     "vs_baseline": None, "dtype": "f64",
                     "data": "synthetic (seeded generators, synth/mpsgen.c)",
-                    "config": {"workload": f"{cfg} {K_NAME[K]}{' CG x500' if cg else ''}{vname}: {CONFIG_DESC[cfg]}",
+                    "config": {"workload": f"{cfg} {K_NAME[K]}"
+                                           f"{(' ' + r['method'].upper() + ' x' + str(r['iters'])) if cg else ''}"
+                                           f"{vname}: {CONFIG_DESC[cfg]}",
                                "precision": K_NAME[K], "order": args.order, "nnz": r["nnz"], "n": r["n"],
                                "parallelism": par,
                                "l2": ("flushed before every timed step: 256 MB write, then 256 MB read of a "
                                       "second buffer") if not cg else "inputs (A, vectors) larger than L2"},
                     "roofline": r["roof"], "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["launches"]}
             if cg:
-                line["config"].update(step="one 500-iteration CG solve (graph-captured batches of 32)",
+                line["config"].update(step=f"one {r['iters']}-iteration {r['method']} solve (graph-captured "
+                                           "batches of 32)",
                                       iterations=r["iterations"], rel_residual=r["rel_residual"],
                                       true_residual=r["true_residual"])
                 line["ms_per_iteration"] = r["per_iter"] * 1e3
