@@ -448,8 +448,8 @@ SolveResult<E> solve_cg(const GpuCsrOperator<MatE, E>& op, const std::vector<E>&
 enum class DotOrder { Tree = MPSG_DOT_TREE, Sequential = MPSG_DOT_SEQUENTIAL };
 
 // Device-resident solve() (krylov.hpp:596-606) and the per-method entry
-// points (solve_bicg :283, solve_cgs :337, solve_bicgstab :398, solve_gpbicg
-// :492).  Reads method, rel_tol, abs_tol, max_iters, x0, lanes_enabled of
+// points (solve_bicg :283, solve_cgs :339, solve_bicgstab :398, solve_gpbicg
+// :478).  Reads method, rel_tol, abs_tol, max_iters, x0, lanes_enabled of
 // SolverConfig; BiCG's transposed products follow the operator's thread count
 // (the reference's per-thread merge) and need a DeviceCsr uploaded with the
 // transpose.  Real, Pure or Mixed mode.

@@ -540,7 +540,7 @@ def solve_bicg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResu
     return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.BiCG)
 
 
-def solve_cgs(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:337
+def solve_cgs(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:339
     return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.CGS)
 
 
@@ -548,7 +548,7 @@ def solve_bicgstab(op: CsrOperator, b, cfg: SolverConfig | None = None) -> Solve
     return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.BiCGSTAB)
 
 
-def solve_gpbicg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:492
+def solve_gpbicg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult:  # krylov.hpp:478
     return _solve_method(op, b, cfg or SolverConfig(), KrylovMethod.GPBiCG)
 
 

@@ -12,7 +12,7 @@
 // Status flow: the posts set KrState::status exactly where the reference
 // returns (close_report), with KrState::k = the iteration count the reference
 // reports, so the residual history always has k + 1 entries.  The half-step
-// exits of BiCGSTAB / GPBiCG (krylov.hpp:449-458, 507-515) pass through
+// exits of BiCGSTAB / GPBiCG (krylov.hpp:424-433, 514-522) pass through
 // KR_HALF: the next launch finishes x and r and then marks Converged.
 #pragma once
 #include <algorithm>
@@ -297,7 +297,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
           store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, load_aos_rw<K>(p, i))));
         });
 
-      case MPSG_BICG:  // krylov.hpp:296-331
+      case MPSG_BICG:  // krylov.hpp:293-330
         if ((e = apply(p, q))) return e;
         if ((e = apply_t(pt, qt))) return e;
         if ((e = L.template reduce<1>(
@@ -329,7 +329,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
           store_aos<K>(pt, i, add(load_aos_rw<K>(rt, i), mul(c.beta, load_aos_rw<K>(pt, i))));
         });
 
-      case MPSG_CGS:  // krylov.hpp:355-392
+      case MPSG_CGS:  // krylov.hpp:350-389
         if ((e = apply(p, v))) return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
@@ -369,7 +369,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
           store_aos<K>(p, i, add(ui, mul(c.beta, add(qi, mul(c.beta, load_aos_rw<K>(p, i))))));
         });
 
-      case MPSG_BICGSTAB: {  // krylov.hpp:433-483; s lives in q
+      case MPSG_BICGSTAB: {  // krylov.hpp:407-469; s lives in q
         double* s_ = q;
         if ((e = apply(p, v))) return e;
         if ((e = L.template reduce<1>(
@@ -380,7 +380,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  post_alpha,
                  KrPf{{rt, v}, 2})))
           return e;
-        // s = r - alpha v; half-step test on ||s|| (:445-458)
+        // s = r - alpha v; half-step test on ||s|| (:421-433)
         if ((e = L.template reduce<1>(
                  GATE_RUN,
                  [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
@@ -392,7 +392,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  KrPf{{r, v}, 2})))
           return e;
         if ((e = apply(s_, t))) return e;
-        // tt = <t, t>; omega = <t, s> / tt (:460-470)
+        // tt = <t, t>; omega = <t, s> / tt (:434-446)
         if ((e = L.template reduce<2>(
                  GATE_RUN,
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
@@ -411,7 +411,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  },
                  KrPf{{t, s_}, 2})))
           return e;
-        // x += alpha p (+ omega s); r = s (- omega t); ||r||, <r~, r> (:450-452, 471-475)
+        // x += alpha p (+ omega s); r = s (- omega t); ||r||, <r~, r> (:426-427, 447-451)
         if ((e = L.template reduce<2>(
                  GATE_RUN_HALF,
                  [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
@@ -433,21 +433,21 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                      return;
                    }
                    if (!kr_record(s, d[0])) return;
-                   // beta = (rho'/rho) (alpha/omega) (:486)
+                   // beta = (rho'/rho) (alpha/omega) (:464-465)
                    s->sc.beta = mul(divide(d[1], s->sc.rho), divide(s->sc.alpha, s->sc.omega));
                    s->sc.rho = d[1];
                    kr_next(s, true);
                  },
                  KrPf{{s_, x, p, t, rt}, 5})))
           return e;
-        // p = r + beta (p - omega v) (:487-488)
+        // p = r + beta (p - omega v) (:466-467)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           const MC<K> pv = sub(load_aos_rw<K>(p, i), mul(c.omega, load_aos_rw<K>(v, i)));
           store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, pv)));
         });
       }
 
-      case MPSG_GPBICG: {  // krylov.hpp:514-588; Ap lives in q, t and t_prev share t
+      case MPSG_GPBICG: {  // krylov.hpp:494-587; Ap lives in q, t and t_prev share t
         double* ap = q;
         if ((e = apply(p, ap))) return e;
         if ((e = L.template reduce<1>(
@@ -458,7 +458,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  post_alpha,
                  KrPf{{rt, ap}, 2})))
           return e;
-        // d = t_prev - r; y = d + alpha (Ap - w); t = r - alpha Ap; half-step test (:529-540)
+        // d = t_prev - r; y = d + alpha (Ap - w); t = r - alpha Ap; half-step test (:507-522)
         if ((e = L.template reduce<1>(
                  GATE_RUN,
                  [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
@@ -474,7 +474,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  KrPf{{t, r, ap, w}, 4})))
           return e;
         if ((e = apply(t, at))) return e;
-        // <At, t>, <At, At>, <y, y>, <y, At>, <y, t>; zeta, eta (:542-567)
+        // <At, t>, <At, At>, <y, y>, <y, At>, <y, t>; zeta, eta (:523-548)
         if ((e = L.template reduce<5>(
                  GATE_RUN,
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
@@ -506,7 +506,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  },
                  KrPf{{at, t, y}, 3})))
           return e;
-        // u, z, x, r; ||r||, <r~, r> (:568-580); half step: x += alpha p, r = t
+        // u, z, x, r; ||r||, <r~, r> (:549-562); half step: x += alpha p, r = t
         if ((e = L.template reduce<2>(
                  GATE_RUN_HALF,
                  [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
@@ -535,7 +535,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                      return;
                    }
                    if (!kr_record(s, d[0])) return;
-                   if (kr_tiny(to_double(s->sc.zeta), s->floor)) {  // (:581-585), after record
+                   if (kr_tiny(to_double(s->sc.zeta), s->floor)) {  // (:575-580), after record
                      kr_break(s, 10);
                      return;
                    }
@@ -545,7 +545,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
                  },
                  KrPf{{t, x, p, r, ap, dv}, 6})))
           return e;
-        // w = At + beta Ap; p = r + beta (p - u); t_prev = t (already in t) (:586-589)
+        // w = At + beta Ap; p = r + beta (p - u); t_prev = t (already in t) (:581-585)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           store_aos<K>(w, i, add(load_aos_rw<K>(at, i), mul(c.beta, load_aos_rw<K>(ap, i))));
           store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, sub(load_aos_rw<K>(p, i), load_aos_rw<K>(u, i)))));

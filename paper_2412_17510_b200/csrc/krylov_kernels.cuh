@@ -127,7 +127,7 @@ MPSG_DI bool kr_record(KrState<K>* st, const MC<K>& d) {
   return true;
 }
 
-// The half-step test of BiCGSTAB / GPBiCG (krylov.hpp:447-449, 505-507):
+// The half-step test of BiCGSTAB / GPBiCG (krylov.hpp:423-424, 513-514):
 // ||s|| = sqrt(d) <= threshold -> KR_HALF with the entry recorded.
 template <int K>
 MPSG_DI void kr_half_test(KrState<K>* st, const MC<K>& d) {
