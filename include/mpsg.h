@@ -285,6 +285,14 @@ MPSG_API int mpsg_dspmv_complex_dev(mpsg_dcsr* A, int order, const double* d_xr_
 MPSG_API int mpsg_dcg(mpsg_dcsr* A, int order, const double* b_local, const double* x0_local,
                       const mpsg_cg_config* cfg, double* x_out_local, double* history, int64_t history_cap,
                       mpsg_cg_report* report);
+/* Row-sharded solve() (krylov.hpp:596-606) for CG, CGS, BiCGSTAB and GPBiCG
+ * (BiCG's transposed product is not sharded: MPSG_E_ARG); arguments as
+ * mpsg_dcg, method / dot order in cfg.  Dots are per-rank partials summed in
+ * rank order, so the sequential dot order is the reference's only at P = 1.
+ * Collective. */
+MPSG_API int mpsg_dsolve(mpsg_dcsr* A, int order, const double* b_local, const double* x0_local,
+                         const mpsg_solver_config* cfg, double* x_out_local, double* history, int64_t history_cap,
+                         mpsg_cg_report* report);
 /* Host-only halo plan: for every peer q, the interval of my rows q reads
  * (send[2q], send[2q+1]) and of q's rows I read (recv[...]); need[2q..] is
  * the column interval rank q reads.  Empty intervals are (0, 0). */

@@ -92,7 +92,7 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
            "mpsg_dcg", "mpsg_halo_plan", "mpsg_csr_upload_ex", "mpsg_sptmv", "mpsg_sptmv_dev",
            "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local", "mpsg_make_vector",
-           "mpsg_sptmv_ex", "mpsg_sptmv_complex_ex", "mpsg_solve")
+           "mpsg_sptmv_ex", "mpsg_sptmv_complex_ex", "mpsg_solve", "mpsg_dsolve")
 
 CSR_COMPLEX, CSR_MIXED, CSR_TRANSPOSE = 1, 2, 4
 
@@ -125,6 +125,8 @@ def lib():
                           ctypes.POINTER(_CgReport)]
     L.mpsg_solve.argtypes = [_P, _P, _i32, _i64, _P, _P, ctypes.POINTER(_SolverConfig), _P, _P, _i64,
                              ctypes.POINTER(_CgReport)]
+    L.mpsg_dsolve.argtypes = [_P, _i32, _P, _P, ctypes.POINTER(_SolverConfig), _P, _P, _i64,
+                              ctypes.POINTER(_CgReport)]
     L.mpsg_partition_rows.argtypes = [_P, _i64, _i32, _P]
     L.mpsg_checksum.argtypes = [_i32, _i64, _P]
     L.mpsg_checksum.restype = _u64
@@ -700,6 +702,36 @@ def dsolve_cg(A: DistCsr, b_local, cfg: SolverConfig | None = None) -> SolveResu
     order = ORDER_FAST if cfg.fast else (ORDER_LANE4 if cfg.lanes_enabled else ORDER_SCALAR)
     A.comm.ctx.check(lib().mpsg_dcg(A.h, order, _p(bb), _p(x0), ctypes.byref(c), _p(x), _p(hist), len(hist),
                                     ctypes.byref(rep)))
+    report = SolverReport(
+        status=SolverStatus(rep.status), converged=bool(rep.converged), detail=rep.detail.decode(),
+        iterations=int(rep.iterations), residual_history=hist[: rep.history_len].tolist(),
+        rhs_norm=rep.rhs_norm, final_recurrence_residual=rep.final_recurrence_residual,
+        final_true_residual=rep.final_true_residual, setup_seconds=rep.setup_seconds,
+        solve_seconds=rep.solve_seconds, device_seconds=rep.device_seconds)
+    return SolveResult(x, report)
+
+
+def dsolve(A: DistCsr, b_local, cfg: SolverConfig | None = None) -> SolveResult:
+    """Row-sharded device solve() (CG, CGS, BiCGSTAB, GPBiCG; cfg.method);
+    b_local / result x are this rank's blocks, the report is identical on
+    every rank.  Collective."""
+    cfg = cfg or SolverConfig()
+    cfg.validate()
+    bb = _aos(b_local, "solver")
+    if bb.shape[0] != A.row_end - A.row_begin:
+        raise ValueError("solver: rhs length does not match the operator")
+    x0 = None
+    if cfg.x0 is not None and len(cfg.x0) > 0:
+        x0 = np.zeros_like(bb)
+        x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)[A.row_begin:A.row_end]
+    c = _SolverConfig(int(cfg.method), max(cfg.threads, 1), cfg.rel_tol, cfg.abs_tol, cfg.max_iters,
+                      cfg.check_every, 1 if cfg.use_graph else 0, DOT_SEQUENTIAL if cfg.exact_dots else DOT_TREE, 0)
+    rep = _CgReport()
+    x = np.empty_like(bb)
+    hist = np.empty(cfg.max_iters + 1)
+    order = ORDER_FAST if cfg.fast else (ORDER_LANE4 if cfg.lanes_enabled else ORDER_SCALAR)
+    A.comm.ctx.check(lib().mpsg_dsolve(A.h, order, _p(bb), _p(x0), ctypes.byref(c), _p(x), _p(hist), len(hist),
+                                       ctypes.byref(rep)))
     report = SolverReport(
         status=SolverStatus(rep.status), converged=bool(rep.converged), detail=rep.detail.decode(),
         iterations=int(rep.iterations), residual_history=hist[: rep.history_len].tolist(),

@@ -794,9 +794,9 @@ int mpsg_solve(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t blen, const 
   if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "solve: unknown order %d", order);
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   switch (A->K) {
-    case 2: return krylov_driver<2>(ctx, A, cfg, order, b, x0, x_out, history, history_cap, report);
-    case 3: return krylov_driver<3>(ctx, A, cfg, order, b, x0, x_out, history, history_cap, report);
-    case 4: return krylov_driver<4>(ctx, A, cfg, order, b, x0, x_out, history, history_cap, report);
+    case 2: return krylov_driver<2>(ctx, A, nullptr, cfg, order, b, x0, x_out, history, history_cap, report);
+    case 3: return krylov_driver<3>(ctx, A, nullptr, cfg, order, b, x0, x_out, history, history_cap, report);
+    case 4: return krylov_driver<4>(ctx, A, nullptr, cfg, order, b, x0, x_out, history, history_cap, report);
   }
   return fail(ctx, MPSG_E_ARG, "solve: unsupported K");
 }

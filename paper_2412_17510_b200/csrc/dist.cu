@@ -419,4 +419,29 @@ int mpsg_dcg(mpsg_dcsr* A, int order, const double* b_local, const double* x0_lo
   return fail(ctx, MPSG_E_ARG, "cg: unsupported K");
 }
 
+int mpsg_dsolve(mpsg_dcsr* A, int order, const double* b_local, const double* x0_local,
+                const mpsg_solver_config* cfg, double* x_out_local, double* history, int64_t history_cap,
+                mpsg_cg_report* report) {
+  if (!A || !cfg || !report || (!b_local && A->row_end > A->row_begin)) return MPSG_E_ARG;
+  mpsg_ctx* ctx = A->comm->ctx;
+  // SolverConfig::validate (krylov.hpp:69-75)
+  if (!(cfg->rel_tol > 0.0) || !(cfg->abs_tol > 0.0))
+    return fail(ctx, MPSG_E_ARG, "solver: tolerances must be positive");
+  if (cfg->max_iters < 1) return fail(ctx, MPSG_E_ARG, "solver: max_iters must be at least 1");
+  if (cfg->threads < 1) return fail(ctx, MPSG_E_ARG, "solver: threads must be at least 1");
+  if (cfg->method < MPSG_CG || cfg->method > MPSG_GPBICG)
+    return fail(ctx, MPSG_E_ARG, "solve: unknown method %d", cfg->method);
+  if (cfg->dot_order != MPSG_DOT_TREE && cfg->dot_order != MPSG_DOT_SEQUENTIAL)
+    return fail(ctx, MPSG_E_ARG, "solve: unknown dot order %d", cfg->dot_order);
+  if (A->cplx) return fail(ctx, MPSG_E_ARG, "solver: complex matrices are not supported");
+  if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "solve: unknown order %d", order);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  switch (A->K) {
+    case 2: return krylov_driver<2>(ctx, A->local, A, cfg, order, b_local, x0_local, x_out_local, history, history_cap, report);
+    case 3: return krylov_driver<3>(ctx, A->local, A, cfg, order, b_local, x0_local, x_out_local, history, history_cap, report);
+    case 4: return krylov_driver<4>(ctx, A->local, A, cfg, order, b_local, x0_local, x_out_local, history, history_cap, report);
+  }
+  return fail(ctx, MPSG_E_ARG, "solve: unsupported K");
+}
+
 }  // extern "C"

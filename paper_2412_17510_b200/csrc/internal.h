@@ -161,7 +161,7 @@ int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, co
 
 // Device solve() driver for one K (krylov_k{2,3,4}.cu).
 template <int K>
-int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cfg, int order,
+int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mpsg_solver_config* cfg, int order,
                   const double* b_host, const double* x0_host, double* x_out, double* history,
                   int64_t history_cap, mpsg_cg_report* rep);
 // Segment bounds of the reference's T-thread sptmv (partition_rows of A's

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "dist.h"
 #include "internal.h"
 #include "krylov_kernels.cuh"
 
@@ -38,6 +39,9 @@ struct KrLauncher {
   int sms;
   int pfd;   // L2 prefetch distance (rounds) of the reductions
   int occ_mode;
+  const mpsg_dcsr* D;  // row-sharded: reductions finish across ranks
+  double* loc;         // [5][K] this rank's totals
+  double* gath;        // [P][5][K]
 
   int check(const char* what) {
     cudaError_t e = cudaGetLastError();
@@ -47,7 +51,7 @@ struct KrLauncher {
   template <int M, class Body, class Post>
   int reduce(int gate, Body body, Post post, KrPf pf = KrPf{{}, 0}) {
     if (seq) {
-      kr_reduce_seq_kernel<K, M><<<1, 1, 0, st>>>(dst, gate, n, body, post);
+      kr_reduce_seq_kernel<K, M><<<1, 1, 0, st>>>(dst, gate, n, body, post, D ? loc : nullptr);
     } else {
       // one resident wave of this kernel (its own occupancy)
       static int occ = -1;
@@ -58,7 +62,13 @@ struct KrLauncher {
       }
       const int o = occ_mode > 0 ? occ_mode : occ;
       const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)G, (int64_t)sms * o));
-      kr_reduce_kernel<K, M><<<g, KR_THREADS, 0, st>>>(dst, gate, n, partial, body, post, pf, pfd);
+      kr_reduce_kernel<K, M><<<g, KR_THREADS, 0, st>>>(dst, gate, n, partial, body, post, pf, pfd,
+                                                       D ? loc : nullptr);
+    }
+    if (D) {
+      int e = allgather_mc(D->comm, loc, gath, M * K, st);
+      if (e) return e;
+      kr_post_gathered_kernel<K, M><<<1, 1, 0, st>>>(dst, gate, gath, D->comm->nranks, post);
     }
     return check("reduction");
   }
@@ -76,13 +86,21 @@ inline double kr_now() {
 // Vector slots (n x K doubles each).
 enum KrVec { V_B, V_X, V_R, V_Q, V_RT, V_P, V_PT, V_QT, V_U, V_V, V_T, V_W, V_Z, V_Y, V_AT, V_D, V_COUNT };
 
+// D != nullptr: row-sharded solve (mpsg_dsolve).  A is this rank's row block
+// (global column indices), b / x0 / x_out its blocks; every vector is
+// allocated global-length with this rank's rows at [row_begin, row_end), so
+// the SpMV inputs get their halo exchanged in place (as the sharded CG), and
+// every reduction is per-rank totals -> allgather -> rank-ordered sum -> post.
 template <int K>
-int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cfg, int order,
+int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mpsg_solver_config* cfg, int order,
                   const double* b_host, const double* x0_host, double* x_out, double* history,
                   int64_t history_cap, mpsg_cg_report* rep) {
   const double t0 = kr_now();
   const int method = cfg->method;
-  const int64_t n = A->nrows;
+  const int64_t n = A->nrows;  // local rows
+  const int64_t nx = D ? D->nglobal : n;
+  const int64_t off = D ? D->row_begin : 0;
+  const int P = D ? D->comm->nranks : 1;
   const size_t vb = (size_t)n * K * sizeof(double);
   cudaStream_t st = ctx->stream;
   const bool seq = cfg->dot_order == MPSG_DOT_SEQUENTIAL;
@@ -98,7 +116,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
   cudaGetLastError();
 
   double* V[V_COUNT] = {};
-  double *part = nullptr, *hist = nullptr, *pend = nullptr;
+  double* Vbase[V_COUNT] = {};
+  double *part = nullptr, *hist = nullptr, *pend = nullptr, *loc = nullptr, *gath = nullptr;
   KrState<K>* dst = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaGraph_t graph = nullptr;
@@ -110,8 +129,10 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
     if (graph) cudaGraphDestroy(graph);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    for (double* v : V)
+    for (double* v : Vbase)
       if (v) cudaFree(v);
+    if (loc) cudaFree(loc);
+    if (gath) cudaFree(gath);
     if (part) cudaFree(part);
     if (hist) cudaFree(hist);
     if (pend) cudaFree(pend);
@@ -146,8 +167,16 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
       {1, 1, 1, 1, 1, 1, 0, 0, 0, 1, 1, 0, 0, 0, 0, 0},  // BiCGSTAB: rt, p, v, s (in Q), t
       {1, 1, 1, 1, 1, 1, 0, 0, 1, 0, 1, 1, 1, 1, 1, 1},  // GPBiCG: rt, p, Ap (in Q), t, w, u, z, y, At, d
   };
+  const size_t vfull = (size_t)nx * K * sizeof(double);
   for (int i = 0; i < V_COUNT; ++i)
-    if (need[method][i]) KR_TRY(cudaMalloc(&V[i], vb ? vb : 8));
+    if (need[method][i]) {
+      KR_TRY(cudaMalloc(&Vbase[i], vfull ? vfull : 8));
+      V[i] = Vbase[i] + off * K;
+    }
+  if (D) {
+    KR_TRY(cudaMalloc(&loc, (size_t)5 * K * sizeof(double)));
+    KR_TRY(cudaMalloc(&gath, (size_t)P * 5 * K * sizeof(double)));
+  }
   KR_TRY(cudaMalloc(&part, (size_t)G * 5 * K * sizeof(double)));
   KR_TRY(cudaMalloc(&hist, (size_t)(max_iters + 1) * sizeof(double)));
   KR_TRY(cudaMalloc(&pend, (size_t)(max_iters + 1) * K * sizeof(double)));
@@ -155,9 +184,18 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
   double *b = V[V_B], *x = V[V_X], *r = V[V_R], *q = V[V_Q], *rt = V[V_RT], *p = V[V_P], *pt = V[V_PT],
          *qt = V[V_QT], *u = V[V_U], *v = V[V_V], *t = V[V_T], *w = V[V_W], *z = V[V_Z], *y = V[V_Y],
          *at = V[V_AT], *dv = V[V_D];
-  KrLauncher<K> L{ctx, st, dst, n, part, G, ub, seq, sms, pfd, occ_mode};
+  KrLauncher<K> L{ctx, st, dst, n, part, G, ub, seq, sms, pfd, occ_mode, D, loc, gath};
   const mpsg_csr* T = A->trans;
-  auto apply = [&](const double* in, double* out) { return launch_spmv(ctx, A, order, in, nullptr, out, nullptr, st); };
+  // y = A v for a vector slot pointer v (this rank's block of a global-length
+  // buffer): halo first when sharded (the SpMV reads global columns)
+  auto apply = [&](double* in, double* out) -> int {
+    double* full = in - off * K;
+    if (D) {
+      int e = halo_exchange(D, full, st);
+      if (e) return e;
+    }
+    return launch_spmv(ctx, A, order, full, nullptr, out, nullptr, st);
+  };
   // CsrOperator::apply_transposed = sptmv at `threads` (krylov.hpp:116-119)
   const int torder = order == MPSG_ORDER_FAST ? MPSG_ORDER_FAST : MPSG_ORDER_SCALAR;
   // the thread-segment bounds apply to the transposed launches only
@@ -169,6 +207,10 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
     return e;
   };
   if (method == MPSG_BICG) {
+    if (D) {
+      cleanup();
+      return fail(ctx, MPSG_E_ARG, "bicg: the transposed product is not available on a row-sharded matrix");
+    }
     if (!T) {
       cleanup();
       return fail(ctx, MPSG_E_ARG, "sptmv: matrix was uploaded without MPSG_CSR_TRANSPOSE");
@@ -567,7 +609,9 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
     const long long remaining = max_iters - done_k;
     const int nb = (int)std::min<long long>(batch, remaining);
     if (nb <= 0) break;
-    if (cfg->use_graph) {
+    // (a single-process group orders ranks with cross-stream events, which a
+    // stream capture cannot record: no graphs there)
+    if (cfg->use_graph && !(D && D->comm->local)) {
       if (nb != gbatch) {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
@@ -660,6 +704,6 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_solver_config* cf
 }  // namespace mpsg
 
 #define MPSG_INSTANTIATE_KRYLOV(K)                                                                         \
-  template int mpsg::krylov_driver<K>(mpsg_ctx*, const mpsg_csr*, const mpsg_solver_config*, int,          \
-                                      const double*, const double*, double*, double*, int64_t,             \
+  template int mpsg::krylov_driver<K>(mpsg_ctx*, const mpsg_csr*, const mpsg_dcsr*, const mpsg_solver_config*, \
+                                      int, const double*, const double*, double*, double*, int64_t,        \
                                       mpsg_cg_report*);

@@ -202,7 +202,7 @@ MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh) {
 template <int K, int M, class Body, class Post>
 __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, int gate, int64_t n,
                                                                double* partial, Body body, Post post, KrPf pf,
-                                                               int pfd) {
+                                                               int pfd, double* local_out) {
   __shared__ MC<K> sh[(KR_THREADS / 32) * M];
   __shared__ bool last;
   if (!gate_open(st->status, gate)) return;
@@ -253,13 +253,21 @@ __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, i
   block_reduce_m<K, M>(s, sh);
   if (threadIdx.x == 0) {
     st->ticket = 0u;
-    post(st, s);
+    if (local_out) {  // row-sharded: this rank's totals, summed across ranks by kr_post_gathered_kernel
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int j = 0; j < K; ++j) local_out[m * K + j] = s[m].c[j];
+    } else {
+      post(st, s);
+    }
   }
 }
 
 // Sequential reduction (one thread, i ascending): the reference's dot order.
 template <int K, int M, class Body, class Post>
-__global__ void kr_reduce_seq_kernel(KrState<K>* st, int gate, int64_t n, Body body, Post post) {
+__global__ void kr_reduce_seq_kernel(KrState<K>* st, int gate, int64_t n, Body body, Post post,
+                                     double* local_out) {
   if (!gate_open(st->status, gate)) return;
   const KrScalars<K> sc = st->sc;
   MC<K> acc[M];
@@ -271,7 +279,29 @@ __global__ void kr_reduce_seq_kernel(KrState<K>* st, int gate, int64_t n, Body b
 #pragma unroll
     for (int m = 0; m < M; ++m) acc[m] = add(acc[m], t[m]);
   }
-  post(st, acc);
+  if (local_out) {
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+      for (int j = 0; j < K; ++j) local_out[m * K + j] = acc[m].c[j];
+  } else {
+    post(st, acc);
+  }
+}
+
+// Row-sharded: the P ranks' totals (allgathered, rank-major [P][M][K]) summed
+// in rank order with the multi-component add, then the post -- the same on
+// every rank, so all ranks take the same decisions.
+template <int K, int M, class Post>
+__global__ void kr_post_gathered_kernel(KrState<K>* st, int gate, const double* gathered, int P, Post post) {
+  if (!gate_open(st->status, gate)) return;
+  MC<K> s[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) s[m] = zero<K>();
+  for (int q = 0; q < P; ++q)
+#pragma unroll
+    for (int m = 0; m < M; ++m) s[m] = add(s[m], load_aos_rw<K>(gathered, (int64_t)q * M + m));
+  post(st, s);
 }
 
 template <int K, class Body>

@@ -191,3 +191,66 @@ def test_sharded_cg_several_ranks(P, K):
     x = np.concatenate([p.x for p in parts])
     assert np.allclose(x[:, 0], xt[:, 0], atol=1e-12)
     assert parts[0].report.final_true_residual <= 10 * single.report.final_true_residual + 1e-30
+
+
+# ---- row-sharded solve() for the other Krylov methods (mpsg_dsolve) ----------------
+@pytest.mark.parametrize("method", ["cg", "cgs", "bicgstab", "gpbicg"])
+def test_one_rank_dsolve_equals_single_gpu_bits(ctx, method):
+    """One rank: the sharded driver is the single-GPU driver plus a one-rank
+    allgather -> identical bits, in both dot orders."""
+    from tests.util import krylov_system
+
+    A, b = krylov_system(200, 3, seed=4, symmetric=method == "cg", density=0.04)
+    for exact in (True, False):
+        cfg = M.SolverConfig(method=M.parse_method(method), rel_tol=1e-40, max_iters=150, exact_dots=exact)
+        single = M.solve(M.CsrOperator(M.DeviceCsr(A, 3, ctx=ctx)), b, cfg)
+        comm = M.Comm(ctx, 1, 0)
+        dA = M.DistCsr.from_global(comm, A, 3)
+        dist = M.dsolve(dA, b, cfg)
+        assert dist.report.residual_history == single.report.residual_history
+        assert bits_equal(dist.x, single.x) and dist.report.status == single.report.status
+        dA.close()
+        comm.close()
+        if exact:  # and, with sequential dots, the reference's solve() itself (C restatement)
+            ref = O.solve(A, b, method, rel_tol=1e-40, max_iters=150)
+            assert bits_equal(np.array(dist.report.residual_history), ref["history"])
+            assert bits_equal(dist.x, ref["x"])
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("method", ["cgs", "bicgstab", "gpbicg", "cg"])
+def test_sharded_solvers_several_ranks(P, method):
+    K = 4 if method in ("bicgstab", "cg") else 2
+    A = synth.config_matrix(5, K, 14)
+    xt = synth.config_vector(5, A.nrows, K)
+    b = O.spmv(A, xt, 1)
+    bounds = M.partition_rows(A.indptr, A.nrows, P)
+    cfg = M.SolverConfig(method=M.parse_method(method), rel_tol=1e-22, max_iters=300)
+
+    def rank_fn(r, comm, ctx):
+        dA = M.DistCsr.from_global(comm, A, K, bounds=bounds)
+        res = M.dsolve(dA, b[dA.row_begin:dA.row_end], cfg)
+        dA.close()
+        return res
+
+    parts = _run_ranks(P, rank_fn)
+    single = M.solve(M.CsrOperator(M.DeviceCsr(A, K)), b, cfg)
+    h0 = parts[0].report.residual_history
+    for p in parts[1:]:  # every rank took the same decisions on the same numbers
+        assert p.report.residual_history == h0 and p.report.iterations == parts[0].report.iterations
+    assert parts[0].report.status == single.report.status == M.SolverStatus.Converged
+    assert abs(parts[0].report.iterations - single.report.iterations) <= max(2, single.report.iterations // 20)
+    x = np.concatenate([p.x for p in parts])
+    assert np.allclose(x[:, 0], xt[:, 0], atol=1e-12)
+    assert parts[0].report.final_true_residual <= 1e-22 * parts[0].report.rhs_norm * 10
+
+
+def test_dsolve_rejects_bicg(ctx):
+    A = synth.config_matrix(5, 2, 6)
+    b = O.spmv(A, synth.config_vector(5, A.nrows, 2), 1)
+    comm = M.Comm(ctx, 1, 0)
+    dA = M.DistCsr.from_global(comm, A, 2)
+    with pytest.raises(M.MpsgError, match="row-sharded"):
+        M.dsolve(dA, b, M.SolverConfig(method=M.KrylovMethod.BiCG))
+    dA.close()
+    comm.close()

@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-for p1 in 10 40; do for K in 4 2; do
-  echo "p1=$p1 $(python tools/kr_probe.py $K cg 64 2 $p1) | $(python tools/kr_probe.py $K bicgstab 32 2 $p1)"
-done; done
+for occ in 0 2 4 6 8 12; do
+  echo "occ=$occ $(MPSG_KR_OCC=$occ python tools/kr_probe.py 4 bicgstab 32) | $(MPSG_KR_OCC=$occ python tools/kr_probe.py 4 cg 64) | $(MPSG_KR_OCC=$occ python tools/kr_probe.py 2 bicgstab 32)"
+done
+python tools/kbench.py cfg1:2:2 cfg5:2:2 cfg4:2:2 cfg1:2:1
+for v in minb14 minb16; do MPSG_LIB=$PWD/variants/$v.so python tools/kbench.py --tag $v cfg1:2:2 cfg5:2:2 cfg4:2:2 cfg1:2:1; done
