@@ -176,7 +176,7 @@ int spmv_host_overlapped(mpsg_ctx* ctx, const mpsg_csr* A, int order, const doub
   return MPSG_OK;
 }
 bool can_overlap(const mpsg_ctx* ctx, const mpsg_csr* A) {
-  return ctx->overlap && ctx->copy && A->part_slice.size() >= 3 && A->part_slice.size() <= 9;
+  return ctx->overlap && ctx->copy && A->part_slice.size() >= 3 && A->part_slice.size() <= 17;
 }
 }  // namespace
 
@@ -326,12 +326,19 @@ int mpsg_csr_upload_ex(mpsg_ctx* ctx, int K, int flags, int64_t nrows, int64_t n
   {
     const int64_t W = std::max<int64_t>(1, ctx->sigma);
     const int64_t nwin = ((int64_t)short_rows.size() + W - 1) / W;
-    const int64_t P = std::min<int64_t>(8, nwin);
+    // P equal parts (env MPSG_PARTS): each part is its own SELL launch, whose
+    // tail costs more than the shorter copy-engine wait of finer parts saves
+    // (config 2 QD end to end: 2 / 4 / 8 / 12 / 16 parts = 22.3 / 23.6 / 21.9 /
+    // 20.3 / 17.9 Gnnz/s; geometric sizes were worse, profiles/r01b_variants.txt).
+    const char* ep = std::getenv("MPSG_PARTS");
+    const int64_t P = std::min<int64_t>(ep ? std::max(2, std::min(16, std::atoi(ep))) : 4, nwin);
     if (P >= 2 && W % C == 0) {
       for (int64_t p = 0; p <= P; ++p) {
         const int64_t w = nwin * p / P;
         A->part_slice.push_back(std::min<int64_t>(w * (W / C), ((int64_t)short_rows.size() + C - 1) / C));
-        A->part_row.push_back(p == 0 ? 0 : (p == P ? nrows : short_rows[(size_t)(w * W)]));
+        A->part_row.push_back(p == 0 ? 0
+                                     : ((p == P || w * W >= (int64_t)short_rows.size()) ? nrows
+                                                                                       : short_rows[(size_t)(w * W)]));
       }
     }
   }

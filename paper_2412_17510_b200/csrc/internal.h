@@ -21,7 +21,7 @@ struct mpsg_ctx {
   cudaStream_t aux = nullptr;     // long-row kernels run here, forked/joined by events
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t copy = nullptr;    // device->host copies overlapped with SpMV parts
-  cudaEvent_t ev_part[8] = {};
+  cudaEvent_t ev_part[16] = {};
   bool overlap = true;            // MPSG_OVERLAP=0 disables
   // transposed product at T > 1 threads: segment bounds of the running call
   // (set by mpsg_sptmv*_ex around the launch; seg_T == 1 means off)
