@@ -481,7 +481,28 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #pragma unroll
   for (int s = 0; s < NS; ++s) acc[s] = zero<K>();
   int64_t k = b + lane;
-  if constexpr (!CPLX) {
+#ifndef MPSG_LONG_MX_U
+#define MPSG_LONG_MX_U 4
+#endif
+  if constexpr (!CPLX && MX && MPSG_LONG_MX_U > 1) {
+    // Mixed (8-byte values): U elements per lane per round, loads in flight
+    // together, added in the lane's element order (same bits as U = 1)
+    constexpr int U = MPSG_LONG_MX_U;
+    for (; k + 32 * (U - 1) < e; k += 32 * U) {
+      int c[U];
+      double a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = ld_s32_stream(L.col + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u] = ld_f64_stream(L.val + k + 32 * u);
+      MC<K> v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = load_aos<K>(xre, c[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[0] = add(acc[0], mul_d(v[u], a[u]));
+    }
+    for (; k < e; k += 32) acc[0] = add(acc[0], mul_d(load_aos<K>(xre, ld_s32_stream(L.col + k)), ld_f64_stream(L.val + k)));
+  } else if constexpr (!CPLX) {
     int c = k < e ? ld_s32_stream(L.col + k) : 0;
     for (; k < e; k += 32) {
       const int cn = k + 32 < e ? ld_s32_stream(L.col + k + 32) : 0;

@@ -26,7 +26,7 @@ K = 2
 A = synth.config_matrix(4, K)
 x = synth.config_vector(4, A.nrows, K)
 mixed = len(sys.argv) > 1 and sys.argv[1] == "mixed"
-for F in (1, 2, 4, 16, 64):
+for F in [int(f) for f in (sys.argv[2] if len(sys.argv) > 2 else "1,2,4,16,64").split(",")]:
     if F == 1:
         B = A
     else:
@@ -52,6 +52,6 @@ for F in (1, 2, 4, 16, 64):
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
     med = statistics.median(ms)
-    print(f"{'mixed' if mixed else 'pure'} fold F={F}: x working set {A.ncols // F * K * 8 / 2**20:.0f} MB, "
+    print(f"{os.environ.get('MPSG_LIB', 'default')[-12:]} {'mixed' if mixed else 'pure'} fold F={F}: x working set {A.ncols // F * K * 8 / 2**20:.0f} MB, "
           f"{med * 1e3:.1f} us, {A.nnz / med / 1e6:.1f} Gnnz/s", flush=True)
     del dA
