@@ -274,6 +274,9 @@ MPSG_API int mpsg_dcsr_upload(mpsg_comm* comm, int K, int is_complex, int64_t ng
 MPSG_API void mpsg_dcsr_destroy(mpsg_dcsr* A);
 /* bounds: nranks+1 entries (may be NULL); halo_rows: rows received per SpMV. */
 MPSG_API int mpsg_dcsr_info(const mpsg_dcsr* A, int64_t* bounds, int64_t* halo_rows);
+/* Rows of this rank whose columns all lie in its own block: they run while
+ * the x halo moves (0 when the rows are not split, e.g. one rank). */
+MPSG_API int mpsg_dcsr_interior_rows(const mpsg_dcsr* A, int64_t* interior_rows);
 /* y_local = (A x)[row block]; x_local / y_local are this rank's blocks.
  * Collective (every rank calls it with the same order). */
 MPSG_API int mpsg_dspmv(mpsg_dcsr* A, int order, const double* x_local, double* y_local);

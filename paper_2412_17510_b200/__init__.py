@@ -92,7 +92,7 @@ EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_s
            "mpsg_dcsr_destroy", "mpsg_dcsr_info", "mpsg_dspmv", "mpsg_dspmv_dev", "mpsg_dspmv_complex_dev",
            "mpsg_dcg", "mpsg_halo_plan", "mpsg_csr_upload_ex", "mpsg_sptmv", "mpsg_sptmv_dev",
            "mpsg_sptmv_complex", "mpsg_sptmv_complex_dev", "mpsg_comm_create_local", "mpsg_make_vector",
-           "mpsg_sptmv_ex", "mpsg_sptmv_complex_ex", "mpsg_solve", "mpsg_dsolve")
+           "mpsg_sptmv_ex", "mpsg_sptmv_complex_ex", "mpsg_solve", "mpsg_dsolve", "mpsg_dcsr_interior_rows")
 
 CSR_COMPLEX, CSR_MIXED, CSR_TRANSPOSE = 1, 2, 4
 
@@ -125,6 +125,7 @@ def lib():
                           ctypes.POINTER(_CgReport)]
     L.mpsg_solve.argtypes = [_P, _P, _i32, _i64, _P, _P, ctypes.POINTER(_SolverConfig), _P, _P, _i64,
                              ctypes.POINTER(_CgReport)]
+    L.mpsg_dcsr_interior_rows.argtypes = [_P, _P]
     L.mpsg_dsolve.argtypes = [_P, _i32, _P, _P, ctypes.POINTER(_SolverConfig), _P, _P, _i64,
                               ctypes.POINTER(_CgReport)]
     L.mpsg_partition_rows.argtypes = [_P, _i64, _i32, _P]
@@ -651,6 +652,12 @@ class DistCsr:
         halo = _i64()
         self.comm.ctx.check(lib().mpsg_dcsr_info(self.h, _p(b), ctypes.byref(halo)))
         return b, int(halo.value)
+
+    def interior_rows(self) -> int:
+        """Rows computed while the x halo moves (columns all in this rank's block)."""
+        v = _i64()
+        self.comm.ctx.check(lib().mpsg_dcsr_interior_rows(self.h, ctypes.byref(v)))
+        return int(v.value)
 
     def close(self):
         if getattr(self, "h", None):

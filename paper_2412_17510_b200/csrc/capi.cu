@@ -86,6 +86,11 @@ __global__ void build_long_kernel(const int* lrow, const int64_t* lptr, const in
   }
 }
 
+__global__ void remap_kernel(int* ids, int64_t n, const int* map) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && ids[i] >= 0) ids[i] = map[ids[i]];
+}
+
 void free_csr(mpsg_csr* A) {
   if (!A) return;
   free_csr(A->trans);
@@ -108,6 +113,25 @@ std::string dim_msg(const char* what, int64_t vsize, int64_t ncols) {
 }  // namespace
 
 namespace mpsg {
+int remap_rows(mpsg_ctx* ctx, mpsg_csr* A, const std::vector<int>& map) {
+  int* d_map = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&d_map, std::max<size_t>(map.size(), 1) * sizeof(int)));
+  cudaStream_t st = ctx->stream;
+  cudaError_t e = cudaMemcpyAsync(d_map, map.data(), map.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+  const int64_t nslots = A->nslices * A->C;
+  if (e == cudaSuccess && nslots > 0)
+    remap_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(A->slot_row, nslots, d_map);
+  if (e == cudaSuccess && A->nlong > 0)
+    remap_kernel<<<(unsigned)((A->nlong + 255) / 256), 256, 0, st>>>(A->lrow, A->nlong, d_map);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_map);
+  if (e != cudaSuccess) return fail(ctx, MPSG_E_CUDA, "remap_rows: %s", cudaGetErrorString(e));
+  A->part_slice.clear();  // host-call output parts index the old rows
+  A->part_row.clear();
+  return MPSG_OK;
+}
+
 int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
                 double* yre, double* yim, cudaStream_t st, bool conj) {
   if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "spmv: unknown order %d", order);
@@ -196,6 +220,9 @@ int mpsg_ctx_create(int device, mpsg_ctx** out) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_side0, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_side1, cudaEventDisableTiming);
   for (auto& ev : ctx->ev_part)
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -237,6 +264,9 @@ void mpsg_ctx_destroy(mpsg_ctx* ctx) {
   for (auto& ev : ctx->ev_part)
     if (ev) cudaEventDestroy(ev);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_side0) cudaEventDestroy(ctx->ev_side0);
+  if (ctx->ev_side1) cudaEventDestroy(ctx->ev_side1);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

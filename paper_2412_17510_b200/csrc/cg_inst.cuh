@@ -109,10 +109,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   using Res = std::integral_constant<int, 2>;
   // q = A p over the global-length p (halo first when sharded)
   auto apply = [&](double* out) -> int {
-    if (D) {
-      int e = halo_exchange(D, pfull, st);
-      if (e) return e;
-    }
+    if (D) return dist_spmv(D, order, pfull, nullptr, out, nullptr, st);  // halo overlapped with interior rows
     return launch_spmv(ctx, A, order, pfull, nullptr, out, nullptr, st);
   };
 

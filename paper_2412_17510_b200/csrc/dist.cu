@@ -121,6 +121,25 @@ int halo_exchange(const mpsg_dcsr* A, double* xfull, cudaStream_t st) {
   return MPSG_OK;
 }
 
+int dist_spmv(const mpsg_dcsr* A, int order, double* xre, double* xim, double* yre, double* yim, cudaStream_t st) {
+  mpsg_ctx* ctx = A->comm->ctx;
+  int rc;
+  if (!A->local_int) {
+    if ((rc = halo_exchange(A, xre, st))) return rc;
+    if (xim && (rc = halo_exchange(A, xim, st))) return rc;
+    return launch_spmv(ctx, A->local, order, xre, xim, yre, yim, st, false);
+  }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side0, st));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_side0, 0));
+  if ((rc = launch_spmv(ctx, A->local_int, order, xre, xim, yre, yim, ctx->side, false))) return rc;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side1, ctx->side));
+  if ((rc = halo_exchange(A, xre, st))) return rc;
+  if (xim && (rc = halo_exchange(A, xim, st))) return rc;
+  if ((rc = launch_spmv(ctx, A->local_bnd, order, xre, xim, yre, yim, st, false))) return rc;
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_side1, 0));
+  return MPSG_OK;
+}
+
 int allgather_mc(const mpsg_comm* c, const double* in, double* out, int K, cudaStream_t st) {
   if (c->nranks == 1 || c->local) {
     CUDA_TRY(c->ctx, cudaMemcpyAsync(out + (size_t)c->rank * K, in, (size_t)K * sizeof(double),
@@ -170,16 +189,19 @@ namespace {
 void free_dcsr(mpsg_dcsr* A) {
   if (!A) return;
   mpsg_csr_destroy(A->local);
+  mpsg_csr_destroy(A->local_int);
+  mpsg_csr_destroy(A->local_bnd);
   for (double* p : {A->xfull[0], A->xfull[1], A->ybuf[0], A->ybuf[1]})
     if (p) cudaFree(p);
   delete A;
 }
 
-// Own block of a distributed vector into the global-length buffer, then halo.
-int stage_x(mpsg_dcsr* A, const double* x_local, double* xfull, cudaMemcpyKind kind, cudaStream_t st) {
+// Own block of a distributed vector into the global-length buffer (the halo
+// follows inside dist_spmv).
+int stage_own(mpsg_dcsr* A, const double* x_local, double* xfull, cudaMemcpyKind kind, cudaStream_t st) {
   const size_t b = (size_t)(A->row_end - A->row_begin) * A->K * sizeof(double);
   if (b) CUDA_TRY(A->comm->ctx, cudaMemcpyAsync(xfull + A->row_begin * A->K, x_local, b, kind, st));
-  return halo_exchange(A, xfull, st);
+  return MPSG_OK;
 }
 
 }  // namespace
@@ -345,6 +367,41 @@ int mpsg_dcsr_upload(mpsg_comm* c, int K, int is_complex, int64_t nglobal, int64
   A->recv.assign((size_t)2 * P, 0);
   mpsg_halo_plan(P, c->rank, A->bounds.data(), A->need.data(), A->send.data(), A->recv.data());
   for (int q = 0; q < P; ++q) A->halo_rows += A->recv[2 * q + 1] - A->recv[2 * q];
+  // interior / boundary split for the halo overlap (MPSG_HALO_OVERLAP=0 disables)
+  const char* eo = std::getenv("MPSG_HALO_OVERLAP");
+  if (P > 1 && (!eo || eo[0] != '0') && A->halo_rows > 0) {
+    std::vector<int> rint, rbnd;
+    for (int64_t i = 0; i < nloc; ++i) {
+      bool inside = true;
+      for (int64_t k = indptr[i]; k < indptr[i + 1] && inside; ++k)
+        inside = indices[k] >= row_begin && indices[k] < row_end;
+      (inside ? rint : rbnd).push_back((int)i);
+    }
+    if (!rint.empty() && !rbnd.empty()) {
+      const int np = (A->cplx ? 2 : 1) * K;
+      auto sub = [&](const std::vector<int>& rows, mpsg_csr** out_csr) -> int {
+        std::vector<int64_t> sp(rows.size() + 1, 0), si;
+        for (size_t r = 0; r < rows.size(); ++r) sp[r + 1] = sp[r] + (indptr[rows[r] + 1] - indptr[rows[r]]);
+        si.reserve((size_t)sp.back());
+        std::vector<std::vector<double>> pl((size_t)np);
+        for (auto& v : pl) v.reserve((size_t)sp.back());
+        for (int row : rows)
+          for (int64_t k = indptr[row]; k < indptr[row + 1]; ++k) {
+            si.push_back(indices[k]);
+            for (int j = 0; j < np; ++j) pl[(size_t)j].push_back(planes[j][k]);
+          }
+        std::vector<const double*> pp((size_t)np);
+        for (int j = 0; j < np; ++j) pp[(size_t)j] = pl[(size_t)j].data();
+        int e = mpsg_csr_upload(ctx, K, is_complex, (int64_t)rows.size(), nglobal, sp.data(), si.data(), pp.data(),
+                                out_csr);
+        if (e) return e;
+        return remap_rows(ctx, *out_csr, rows);
+      };
+      if ((rc = sub(rint, &A->local_int))) return rc;
+      if ((rc = sub(rbnd, &A->local_bnd))) return rc;
+      A->n_interior = (int64_t)rint.size();
+    }
+  }
   const size_t xb = (size_t)std::max<int64_t>(nglobal, 1) * K * sizeof(double);
   for (int j = 0; j < (A->cplx ? 2 : 1); ++j) {
     CUDA_TRY(ctx, cudaMalloc(&A->xfull[j], xb));
@@ -363,13 +420,19 @@ int mpsg_dcsr_info(const mpsg_dcsr* A, int64_t* bounds, int64_t* halo_rows) {
   return MPSG_OK;
 }
 
+int mpsg_dcsr_interior_rows(const mpsg_dcsr* A, int64_t* interior_rows) {
+  if (!A || !interior_rows) return MPSG_E_ARG;
+  *interior_rows = A->n_interior;
+  return MPSG_OK;
+}
+
 int mpsg_dspmv_dev(mpsg_dcsr* A, int order, const double* d_x_local, double* d_y_local, void* stream) {
   if (!A) return MPSG_E_ARG;
   if (A->cplx) return fail(A->comm->ctx, MPSG_E_ARG, "dspmv: matrix is complex, use mpsg_dspmv_complex_dev");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : A->comm->ctx->stream;
-  int rc = stage_x(A, d_x_local, A->xfull[0], cudaMemcpyDeviceToDevice, st);
+  int rc = stage_own(A, d_x_local, A->xfull[0], cudaMemcpyDeviceToDevice, st);
   if (rc) return rc;
-  return launch_spmv(A->comm->ctx, A->local, order, A->xfull[0], nullptr, d_y_local, nullptr, st);
+  return dist_spmv(A, order, A->xfull[0], nullptr, d_y_local, nullptr, st);
 }
 
 int mpsg_dspmv_complex_dev(mpsg_dcsr* A, int order, const double* d_xr_local, const double* d_xi_local,
@@ -377,10 +440,10 @@ int mpsg_dspmv_complex_dev(mpsg_dcsr* A, int order, const double* d_xr_local, co
   if (!A) return MPSG_E_ARG;
   if (!A->cplx) return fail(A->comm->ctx, MPSG_E_ARG, "dspmv_complex: matrix is real");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : A->comm->ctx->stream;
-  int rc = stage_x(A, d_xr_local, A->xfull[0], cudaMemcpyDeviceToDevice, st);
-  if (!rc) rc = stage_x(A, d_xi_local, A->xfull[1], cudaMemcpyDeviceToDevice, st);
+  int rc = stage_own(A, d_xr_local, A->xfull[0], cudaMemcpyDeviceToDevice, st);
+  if (!rc) rc = stage_own(A, d_xi_local, A->xfull[1], cudaMemcpyDeviceToDevice, st);
   if (rc) return rc;
-  return launch_spmv(A->comm->ctx, A->local, order, A->xfull[0], A->xfull[1], d_yr_local, d_yi_local, st);
+  return dist_spmv(A, order, A->xfull[0], A->xfull[1], d_yr_local, d_yi_local, st);
 }
 
 int mpsg_dspmv(mpsg_dcsr* A, int order, const double* x_local, double* y_local) {
@@ -393,9 +456,9 @@ int mpsg_dspmv(mpsg_dcsr* A, int order, const double* x_local, double* y_local) 
   for (int j = 0; j < ns; ++j)
     if (!A->ybuf[j]) CUDA_TRY(ctx, cudaMalloc(&A->ybuf[j], b ? b : 8));
   cudaStream_t st = ctx->stream;
-  int rc = stage_x(A, x_local, A->xfull[0], cudaMemcpyHostToDevice, st);
+  int rc = stage_own(A, x_local, A->xfull[0], cudaMemcpyHostToDevice, st);
   if (rc) return rc;
-  if ((rc = launch_spmv(ctx, A->local, order, A->xfull[0], nullptr, A->ybuf[0], nullptr, st))) return rc;
+  if ((rc = dist_spmv(A, order, A->xfull[0], nullptr, A->ybuf[0], nullptr, st))) return rc;
   if (b) CUDA_TRY(ctx, cudaMemcpyAsync(y_local, A->ybuf[0], b, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   return MPSG_OK;

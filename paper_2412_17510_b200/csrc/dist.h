@@ -77,6 +77,11 @@ struct mpsg_comm {
 struct mpsg_dcsr {
   mpsg_comm* comm = nullptr;
   mpsg_csr* local = nullptr;  // this rank's rows, global column indices
+  // the same rows split for the halo overlap: interior rows (every column in
+  // this rank's block) run while the halo moves, boundary rows after it
+  mpsg_csr* local_int = nullptr;
+  mpsg_csr* local_bnd = nullptr;
+  int64_t n_interior = 0;
   int K = 2;
   bool cplx = false;
   int64_t nglobal = 0, row_begin = 0, row_end = 0;
@@ -100,6 +105,10 @@ namespace mpsg {
 
 // Exchange the halo of a global-length buffer whose own block is in place.
 int halo_exchange(const mpsg_dcsr* A, double* xfull, cudaStream_t st);
+// y = A x for a sharded matrix, x's own block in place in the global-length
+// xfull buffers: interior rows on ctx->side concurrently with the halo
+// exchange, then boundary rows (or halo + all rows when not split).
+int dist_spmv(const mpsg_dcsr* A, int order, double* xre, double* xim, double* yre, double* yim, cudaStream_t st);
 // out[P*K] = every rank's in[K] (rank order).
 int allgather_mc(const mpsg_comm* c, const double* in, double* out, int K, cudaStream_t st);
 // Host allgather of n int64 per rank (setup only).

@@ -21,6 +21,8 @@ struct mpsg_ctx {
   cudaStream_t aux = nullptr;     // long-row kernels run here, forked/joined by events
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t copy = nullptr;    // device->host copies overlapped with SpMV parts
+  cudaStream_t side = nullptr;    // sharded SpMV: interior rows while the x halo moves
+  cudaEvent_t ev_side0 = nullptr, ev_side1 = nullptr;
   cudaEvent_t ev_part[16] = {};
   bool overlap = true;            // MPSG_OVERLAP=0 disables
   // transposed product at T > 1 threads: segment bounds of the running call
@@ -153,6 +155,9 @@ int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, 
 // part >= 0 the SELL slices of output part `part` (A->part_slice).
 int launch_spmv_part(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
                      double* yre, double* yim, cudaStream_t st, bool conj, int part);
+// Output rows of an uploaded matrix renumbered: row i of the uploaded CSR
+// writes y[map[i]] (a row subset of a larger matrix; capi.cu).
+int remap_rows(mpsg_ctx* ctx, mpsg_csr* A, const std::vector<int>& map);
 // Device CG driver for one K (cg_k{2,3,4}.cu).
 template <int K>
 int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, const double* x0,

@@ -190,10 +190,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
   // buffer): halo first when sharded (the SpMV reads global columns)
   auto apply = [&](double* in, double* out) -> int {
     double* full = in - off * K;
-    if (D) {
-      int e = halo_exchange(D, full, st);
-      if (e) return e;
-    }
+    if (D) return dist_spmv(D, order, full, nullptr, out, nullptr, st);  // halo overlapped with interior rows
     return launch_spmv(ctx, A, order, full, nullptr, out, nullptr, st);
   };
   // CsrOperator::apply_transposed = sptmv at `threads` (krylov.hpp:116-119)
