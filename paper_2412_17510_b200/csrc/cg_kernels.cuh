@@ -21,9 +21,7 @@
 namespace mpsg {
 
 constexpr int CG_RUNNING = -1;
-#ifndef MPSG_CG_PIPE
-#define MPSG_CG_PIPE 1
-#endif
+
 #ifndef MPSG_DOT_THREADS
 #define MPSG_DOT_THREADS 256
 #endif
@@ -220,7 +218,6 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
       return mul(w, w);
     }
   };
-#if MPSG_CG_PIPE
   if constexpr (MODE == 0) {
     // register double buffer: the next round's operands are in flight while
     // this round's product is accumulated
@@ -261,9 +258,9 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
       store_aos<K>(r, i, ri);
       acc = add(acc, mul(ri, ri));
     }
-  } else
-#endif
-  for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) acc = add(acc, term(i));
+  } else {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) acc = add(acc, term(i));
+  }
   reduce_finish<K, DOT_THREADS>(st, post, acc, partial, local_out, sh);
 }
 

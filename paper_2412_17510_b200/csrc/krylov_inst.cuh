@@ -37,8 +37,7 @@ struct KrLauncher {
   int ub;    // map grid
   bool seq;  // reference dot order (one thread)
   int sms;
-  int pfd;   // L2 prefetch distance (rounds) of the reductions
-  int occ_mode;
+  int occ_mode;  // blocks per SM of the reduction grid (0: the kernel's occupancy; MPSG_KR_OCC)
   const mpsg_dcsr* D;  // row-sharded: reductions finish across ranks
   double* loc;         // [5][K] this rank's totals
   double* gath;        // [P][5][K]
@@ -49,7 +48,7 @@ struct KrLauncher {
                                              cudaGetErrorString(e));
   }
   template <int M, class Body, class Post>
-  int reduce(int gate, Body body, Post post, KrPf pf = KrPf{{}, 0}) {
+  int reduce(int gate, Body body, Post post) {
     if (seq) {
       kr_reduce_seq_kernel<K, M><<<1, 1, 0, st>>>(dst, gate, n, body, post, D ? loc : nullptr);
     } else {
@@ -62,8 +61,7 @@ struct KrLauncher {
       }
       const int o = occ_mode > 0 ? occ_mode : occ;
       const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)G, (int64_t)sms * o));
-      kr_reduce_kernel<K, M><<<g, KR_THREADS, 0, st>>>(dst, gate, n, partial, body, post, pf, pfd,
-                                                       D ? loc : nullptr);
+      kr_reduce_kernel<K, M><<<g, KR_THREADS, 0, st>>>(dst, gate, n, partial, body, post, D ? loc : nullptr);
     }
     if (D) {
       int e = allgather_mc(D->comm, loc, gath, M * K, st);
@@ -107,9 +105,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)KR_MAX_BLOCKS, (n + KR_THREADS - 1) / KR_THREADS));
-  const char* e_pf = std::getenv("MPSG_KR_PF");
   const char* e_occ = std::getenv("MPSG_KR_OCC");
-  const int pfd = e_pf ? std::atoi(e_pf) : 0;
   const int occ_mode = e_occ ? std::atoi(e_occ) : 0;
   const int ub = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, (n + 255) / 256));
   const int64_t max_iters = cfg->max_iters;
@@ -184,7 +180,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
   double *b = V[V_B], *x = V[V_X], *r = V[V_R], *q = V[V_Q], *rt = V[V_RT], *p = V[V_P], *pt = V[V_PT],
          *qt = V[V_QT], *u = V[V_U], *v = V[V_V], *t = V[V_T], *w = V[V_W], *z = V[V_Z], *y = V[V_Y],
          *at = V[V_AT], *dv = V[V_D];
-  KrLauncher<K> L{ctx, st, dst, n, part, G, ub, seq, sms, pfd, occ_mode, D, loc, gath};
+  KrLauncher<K> L{ctx, st, dst, n, part, G, ub, seq, sms, occ_mode, D, loc, gath};
   const mpsg_csr* T = A->trans;
   // y = A v for a vector slot pointer v (this rank's block of a global-length
   // buffer): halo first when sharded (the SpMV reads global columns)
@@ -312,8 +308,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(p, i), load_aos_rw<K>(q, i));  // sigma = <p, q>
                  },
-                 post_alpha,
-                 KrPf{{p, q}, 2})))
+                 post_alpha)))
           return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
@@ -329,8 +324,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    s->sc.beta = divide(d[0], s->sc.rho);
                    s->sc.rho = d[0];
                    kr_next(s, false);
-                 },
-                 KrPf{{x, p, r, q}, 4})))
+                 })))
           return e;
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, load_aos_rw<K>(p, i))));
@@ -344,8 +338,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(pt, i), load_aos_rw<K>(q, i));  // sigma = <p~, q>
                  },
-                 post_alpha,
-                 KrPf{{pt, q}, 2})))
+                 post_alpha)))
           return e;
         if ((e = L.template reduce<2>(
                  GATE_RUN,
@@ -360,8 +353,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    d[0] = mul(ri, ri);   // ||r||^2
                    d[1] = mul(rti, ri);  // rho' = <r~, r>
                  },
-                 post_rho_next,
-                 KrPf{{x, p, r, q, rt, qt}, 6})))
+                 post_rho_next)))
           return e;
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, load_aos_rw<K>(p, i))));
@@ -375,8 +367,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i));  // sigma = <r~, v>
                  },
-                 post_alpha,
-                 KrPf{{rt, v}, 2})))
+                 post_alpha)))
           return e;
         // q = u - alpha v; t = u + q; x += alpha t
         if ((e = L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
@@ -397,8 +388,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    d[0] = mul(ri, ri);
                    d[1] = mul(load_aos_rw<K>(rt, i), ri);
                  },
-                 post_rho_next,
-                 KrPf{{r, w, rt}, 3})))
+                 post_rho_next)))
           return e;
         // u = r + beta q; p = u + beta (q + beta p)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
@@ -416,8 +406,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i));  // sigma = <r~, v>
                  },
-                 post_alpha,
-                 KrPf{{rt, v}, 2})))
+                 post_alpha)))
           return e;
         // s = r - alpha v; half-step test on ||s|| (:421-433)
         if ((e = L.template reduce<1>(
@@ -427,8 +416,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    store_aos<K>(s_, i, si);
                    d[0] = mul(si, si);
                  },
-                 [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); },
-                 KrPf{{r, v}, 2})))
+                 [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); })))
           return e;
         if ((e = apply(s_, t))) return e;
         // tt = <t, t>; omega = <t, s> / tt (:434-446)
@@ -447,8 +435,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    const MC<K> om = divide(d[1], d[0]);
                    s->sc.omega = om;
                    if (kr_tiny(to_double(om), s->floor)) kr_break(s, 7);
-                 },
-                 KrPf{{t, s_}, 2})))
+                 })))
           return e;
         // x += alpha p (+ omega s); r = s (- omega t); ||r||, <r~, r> (:426-427, 447-451)
         if ((e = L.template reduce<2>(
@@ -476,8 +463,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    s->sc.beta = mul(divide(d[1], s->sc.rho), divide(s->sc.alpha, s->sc.omega));
                    s->sc.rho = d[1];
                    kr_next(s, true);
-                 },
-                 KrPf{{s_, x, p, t, rt}, 5})))
+                 })))
           return e;
         // p = r + beta (p - omega v) (:466-467)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
@@ -494,8 +480,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                  [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
                    d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(ap, i));  // sigma = <r~, Ap>
                  },
-                 post_alpha,
-                 KrPf{{rt, ap}, 2})))
+                 post_alpha)))
           return e;
         // d = t_prev - r; y = d + alpha (Ap - w); t = r - alpha Ap; half-step test (:507-522)
         if ((e = L.template reduce<1>(
@@ -509,8 +494,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    store_aos<K>(t, i, ti);
                    d[0] = mul(ti, ti);
                  },
-                 [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); },
-                 KrPf{{t, r, ap, w}, 4})))
+                 [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); })))
           return e;
         if ((e = apply(t, at))) return e;
         // <At, t>, <At, At>, <y, y>, <y, At>, <y, t>; zeta, eta (:523-548)
@@ -542,8 +526,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                      s->sc.zeta = divide(sub(mul(yy, att), mul(yt, yat)), den);
                      s->sc.eta = divide(sub(mul(ata, yt), mul(yat, att)), den);
                    }
-                 },
-                 KrPf{{at, t, y}, 3})))
+                 })))
           return e;
         // u, z, x, r; ||r||, <r~, r> (:549-562); half step: x += alpha p, r = t
         if ((e = L.template reduce<2>(
@@ -581,8 +564,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    s->sc.beta = mul(divide(s->sc.alpha, s->sc.zeta), divide(d[1], s->sc.rho));
                    s->sc.rho = d[1];
                    kr_next(s, true);
-                 },
-                 KrPf{{t, x, p, r, ap, dv}, 6})))
+                 })))
           return e;
         // w = At + beta Ap; p = r + beta (p - u); t_prev = t (already in t) (:581-585)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {

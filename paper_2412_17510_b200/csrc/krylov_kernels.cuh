@@ -61,21 +61,6 @@ struct KrState {
   unsigned ticket;    // last-block arrival counter (self-resetting)
 };
 
-// Vectors a reduction body reads, prefetched into L2 `pfd` rounds ahead of
-// use (prefetch.global.L2: no registers held, unlike a register pipeline),
-// so the per-thread accumulation chain does not wait on DRAM every round.
-struct KrPf {
-  const double* p[6];
-  int n;
-};
-
-MPSG_DI void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-
-template <int K>
-MPSG_DI void kr_prefetch(const KrPf& pf, int64_t j) {
-  for (int v = 0; v < pf.n; ++v) prefetch_l2(pf.p[v] + j * K);
-}
-
 MPSG_DI bool gate_open(int status, int gate) {
   return gate == GATE_ALWAYS || status == KR_RUNNING || (gate == GATE_RUN_HALF && status == KR_HALF);
 }
@@ -201,8 +186,8 @@ MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh) {
 // and runs post(st, totals).  Deterministic for a fixed grid.
 template <int K, int M, class Body, class Post>
 __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, int gate, int64_t n,
-                                                               double* partial, Body body, Post post, KrPf pf,
-                                                               int pfd, double* local_out) {
+                                                               double* partial, Body body, Post post,
+                                                               double* local_out) {
   __shared__ MC<K> sh[(KR_THREADS / 32) * M];
   __shared__ bool last;
   if (!gate_open(st->status, gate)) return;
@@ -214,11 +199,7 @@ __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, i
   MC<K> acc[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) acc[m] = zero<K>();
-  if (pfd > 0)
-    for (int d = 1; d <= pfd; ++d)
-      if (lo + threadIdx.x + (int64_t)d * KR_THREADS < hi) kr_prefetch<K>(pf, lo + threadIdx.x + (int64_t)d * KR_THREADS);
   for (int64_t i = lo + threadIdx.x; i < hi; i += KR_THREADS) {
-    if (pfd > 0 && i + (int64_t)pfd * KR_THREADS < hi) kr_prefetch<K>(pf, i + (int64_t)pfd * KR_THREADS);
     MC<K> t[M];
     body(sc, i, t);
 #pragma unroll
