@@ -52,13 +52,13 @@ struct KrLauncher {
     if (seq) {
       kr_reduce_seq_kernel<K, M><<<1, 1, 0, st>>>(dst, gate, n, body, post, D ? loc : nullptr);
     } else {
-      // one resident wave of this kernel (its own occupancy)
-      static int occ = -1;
-      if (occ < 0) {
-        occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kr_reduce_kernel<K, M, Body, Post>, KR_THREADS, 0);
-        if (occ < 1) occ = 1;
-      }
+      // one resident wave of this kernel (its own occupancy; a thread-safe
+      // static: ranks of a single-process group solve on several host threads)
+      static const int occ = [] {
+        int o = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kr_reduce_kernel<K, M, Body, Post>, KR_THREADS, 0);
+        return o < 1 ? 1 : o;
+      }();
       const int o = occ_mode > 0 ? occ_mode : occ;
       const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)G, (int64_t)sms * o));
       kr_reduce_kernel<K, M><<<g, KR_THREADS, 0, st>>>(dst, gate, n, partial, body, post, D ? loc : nullptr);
