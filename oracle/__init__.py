@@ -74,6 +74,9 @@ def orc():
         L.orc_solve.argtypes = [_i32, _i32, _i32, _i32, _i64, _P, _P, _P, _P, _P, _f64, _f64, _i64, _P, _P,
                                 _P, _P, _P, _P, _P]
         L.orc_solve.restype = _i32
+        L.orc_solve_ex.argtypes = [_i32, _i32, _i32, _i32, _i32, _i64, _P, _P, _P, _P, _P, _f64, _f64, _i64, _P,
+                                   _P, _P, _P, _P, _P, _P]
+        L.orc_solve_ex.restype = _i32
         _orc = L
     return _orc
 
@@ -210,9 +213,10 @@ def detail_text(method, reason: int) -> str:
 
 
 def solve(A, b, method="bicgstab", order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters=10000,
-          x0=None):
+          x0=None, mixed=False):
     """C restatement of solve() (krylov.hpp:596-606): every method, sequential
-    dots, CsrOperator products (sptmv at `threads`)."""
+    dots, CsrOperator products (sptmv at `threads`); mixed: A is the binary64
+    matrix of CsrOperator<double> (one plane, mul_by_double products)."""
     K = b.shape[1]
     n = A.nrows
     x = np.zeros((n, K))
@@ -221,8 +225,9 @@ def solve(A, b, method="bicgstab", order=LANE4, threads=1, rel_tol=1e-13, abs_to
     status, reason = np.zeros(1, np.int32), np.zeros(1, np.int32)
     rhs, tr = np.zeros(1), np.zeros(1)
     x0a = None if x0 is None else np.ascontiguousarray(np.asarray(x0, np.float64))
-    nh = orc().orc_solve(_method_id(method), K, order, threads, n, _p(_c(A.indptr, np.int64)),
-                         _p(_c(A.indices, np.int64)), _p(_c(A.planes[:K])), _p(_c(b)),
+    nh = orc().orc_solve_ex(_method_id(method), K, order, threads, 1 if mixed else 0, n,
+                            _p(_c(A.indptr, np.int64)), _p(_c(A.indices, np.int64)),
+                            _p(_c(A.planes[:1] if mixed else A.planes[:K])), _p(_c(b)),
                          None if x0a is None else _p(x0a), rel_tol, abs_tol, max_iters, _p(x), _p(hist),
                          _p(iters), _p(status), _p(reason), _p(rhs), _p(tr))
     if nh < 0:
@@ -474,10 +479,11 @@ def ref_cg(A, b, order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters
 
 
 def ref_solve(A, b, method="bicgstab", order=LANE4, threads=1, rel_tol=1e-13, abs_tol=1e-99, max_iters=10000,
-              x0=None):
-    """The reference solve() itself (oracle/_ref) on the same inputs."""
+              x0=None, mixed=False):
+    """The reference solve() itself (oracle/_ref) on the same inputs (mixed:
+    CsrOperator<double> over A's leading plane)."""
     K = b.shape[1]
-    Ah, bh = RefCsr(A, K), RefVec(b)
+    Ah, bh = RefCsr(A, K, mixed), RefVec(b)
     x = np.zeros((A.nrows, K))
     hist = np.zeros(max_iters + 2)
     iters = np.zeros(1, np.int64)

@@ -664,13 +664,14 @@ typedef struct {
   double thr[4], cap, floor;
   double *hist;
   int64_t nh;
+  int mixed; /* CsrOperator<double> with K-component vectors (bench.cpp:550-557) */
 } KrCtx;
 
 static void kr_apply(const KrCtx *c, const double *x, double *y) {
-  orc_spmv(c->K, c->lanes, 0, c->n, c->n, c->n, c->indptr, c->indices, c->vals, x, y);
+  orc_spmv(c->K, c->lanes, c->mixed, c->n, c->n, c->n, c->indptr, c->indices, c->vals, x, y);
 }
 static void kr_apply_t(const KrCtx *c, const double *x, double *y) {
-  orc_sptmv(c->K, 0, c->threads, c->n, c->n, c->n, c->indptr, c->indices, c->vals, x, y);
+  orc_sptmv(c->K, c->mixed, c->threads, c->n, c->n, c->n, c->indptr, c->indices, c->vals, x, y);
 }
 static void kr_axpy(int K, int64_t n, const double *alpha, const double *x, double *y) {
   double t[4];
@@ -1065,13 +1066,31 @@ out:
 /* solve() (krylov.hpp:596-606).  x0 may be NULL (zero start).  history needs
  * max_iters + 1 entries.  Returns the history length, or -1 on a config error
  * (SolverConfig::validate, krylov.hpp:69-75). */
+ORC_API int orc_solve_ex(int method, int K, int lanes, int threads, int mixed, int64_t n, const int64_t *indptr,
+                         const int64_t *indices, const double *vals, const double *b, const double *x0,
+                         double rel_tol, double abs_tol, int64_t max_iters, double *x, double *history,
+                         int64_t *iterations, int *status, int *reason, double *rhs_norm,
+                         double *final_true_residual);
+
 ORC_API int orc_solve(int method, int K, int lanes, int threads, int64_t n, const int64_t *indptr,
                       const int64_t *indices, const double *vals, const double *b, const double *x0,
                       double rel_tol, double abs_tol, int64_t max_iters, double *x, double *history,
                       int64_t *iterations, int *status, int *reason, double *rhs_norm,
                       double *final_true_residual) {
+  return orc_solve_ex(method, K, lanes, threads, 0, n, indptr, indices, vals, b, x0, rel_tol, abs_tol, max_iters,
+                      x, history, iterations, status, reason, rhs_norm, final_true_residual);
+}
+
+/* mixed != 0: vals is the binary64 matrix (one plane), products mul_by_double
+ * (Mixed mode, kernels.hpp:55-58) -- solve() over CsrOperator<double>. */
+ORC_API int orc_solve_ex(int method, int K, int lanes, int threads, int mixed, int64_t n, const int64_t *indptr,
+                         const int64_t *indices, const double *vals, const double *b, const double *x0,
+                         double rel_tol, double abs_tol, int64_t max_iters, double *x, double *history,
+                         int64_t *iterations, int *status, int *reason, double *rhs_norm,
+                         double *final_true_residual) {
   if (!(rel_tol > 0.0) || !(abs_tol > 0.0) || max_iters < 1 || method < 0 || method > 4) return -1;
-  KrCtx c = {K, lanes, threads < 1 ? 1 : threads, n, indptr, indices, vals, {0, 0, 0, 0}, 0, 0, history, 0};
+  KrCtx c = {K, lanes, threads < 1 ? 1 : threads, n, indptr, indices, vals, {0, 0, 0, 0}, 0, 0, history, 0,
+             mixed ? 1 : 0};
   KR_VEC(r);
   KR_VEC(q);
   double t[4], bn[4], tmp[4], r0[4];

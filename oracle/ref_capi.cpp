@@ -348,7 +348,8 @@ int64_t ref_cg(void* A, void* b, int lanes, int threads, double rel_tol, double 
         [&](auto& mat, auto& vec) {
           using E = std::decay_t<decltype(mat.values.get(0))>;
           using F = typename std::decay_t<decltype(vec)>::value_type;
-          if constexpr (std::is_same_v<E, F>) {
+          // Pure (E == F) or Mixed (E = double: CsrOperator<double>, bench.cpp:550-557)
+          if constexpr (std::is_same_v<E, F> || (std::is_same_v<E, double> && !std::is_same_v<F, double>)) {
             CsrOperator<E> op{&mat, threads, lanes != 0};
             SolverConfig cfg;
             cfg.method = KrylovMethod::CG;
@@ -394,7 +395,8 @@ int64_t ref_solve(void* A, void* b, int method, int lanes, int threads, double r
         [&](auto& mat, auto& vec) {
           using E = std::decay_t<decltype(mat.values.get(0))>;
           using F = typename std::decay_t<decltype(vec)>::value_type;
-          if constexpr (std::is_same_v<E, F>) {
+          // Pure (E == F) or Mixed (E = double: CsrOperator<double>, bench.cpp:550-557)
+          if constexpr (std::is_same_v<E, F> || (std::is_same_v<E, double> && !std::is_same_v<F, double>)) {
             CsrOperator<E> op{&mat, threads, lanes != 0};
             SolverConfig cfg;
             cfg.method = static_cast<KrylovMethod>(method);

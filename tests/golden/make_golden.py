@@ -227,6 +227,20 @@ def krylov_small():
     return out
 
 
+def krylov_mixed():
+    """The reference solve() over CsrOperator<double> (Mixed mode)."""
+    from tests.util import krylov_mixed_cases
+
+    out = {}
+    for name, A, b, m, kw in krylov_mixed_cases():
+        r = O.ref_solve(A, b, m, mixed=True, **kw)
+        out[f"{name}_history"] = r["history"]
+        out[f"{name}_x"] = r["x"]
+        out[f"{name}_meta"] = np.array([r["iterations"], r["status"], r["rhs_norm"], r["final_true_residual"]])
+        out[f"{name}_detail"] = np.array(r["detail"])
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cg-full", action="store_true")
@@ -234,7 +248,7 @@ def main():
     a = ap.parse_args()
     assert O.ref_available(), "build the reference first: make -C oracle ref"
     jobs = {"arith": arith, "spmv_small": spmv_small, "spmv_full": spmv_full, "cg_small": cg_small,
-            "mixed_sptmv": mixed_sptmv, "krylov_small": krylov_small}
+            "mixed_sptmv": mixed_sptmv, "krylov_small": krylov_small, "krylov_mixed": krylov_mixed}
     if a.cg_full:
         jobs = {"cg_full": cg_full}
     for name, fn in jobs.items():

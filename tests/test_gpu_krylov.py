@@ -134,3 +134,24 @@ def test_solve_errors(ctx):
     # the default method is BiCGSTAB (krylov.hpp:59)
     assert M.SolverConfig().method == M.KrylovMethod.BiCGSTAB
     assert str(M.KrylovMethod.GPBiCG) == "gpbicg" and M.parse_method("cgs") == M.KrylovMethod.CGS
+
+
+# ---- Mixed mode: solve() over CsrOperator<double> with K-component vectors ------
+from tests.util import krylov_mixed_cases  # noqa: E402
+
+_MCASES = krylov_mixed_cases()
+
+
+@pytest.mark.parametrize("case", _MCASES, ids=[c[0] for c in _MCASES])
+def test_mixed_solve_exact_dots_bit_equal_reference(ctx, case):
+    name, Am, b, m, kw = case
+    g = golden("krylov_mixed")
+    K = b.shape[1]
+    dA = M.DeviceCsr(Am, K, ctx=ctx, mixed=True, transpose=(m == "bicg"))
+    op = M.CsrOperator(dA, threads=kw.get("threads", 1))
+    res = M.solve(op, b, M.SolverConfig(method=M.parse_method(m), exact_dots=True))
+    meta = g[f"{name}_meta"]
+    assert (res.report.iterations, int(res.report.status)) == (int(meta[0]), int(meta[1]))
+    assert bits_equal(np.array(res.report.residual_history), g[f"{name}_history"])
+    assert bits_equal(res.x, g[f"{name}_x"])
+    assert res.report.final_true_residual == meta[3] and res.report.detail == str(g[f"{name}_detail"])

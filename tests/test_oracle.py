@@ -280,3 +280,21 @@ def test_oracle_solver_rejects_bad_config():
         O.solve(A, b, "cg", rel_tol=0.0)
     with pytest.raises(ValueError):
         O.solve(A, b, "cg", max_iters=0)
+
+
+# ---- Mixed-mode solve() (CsrOperator<double>, bench.cpp:550-557) --------------
+from tests.util import krylov_mixed_cases  # noqa: E402
+
+_MCASES = krylov_mixed_cases()
+
+
+@pytest.mark.parametrize("case", _MCASES, ids=[c[0] for c in _MCASES])
+def test_oracle_mixed_solvers_equal_reference_golden(case):
+    name, A, b, m, kw = case
+    g = golden("krylov_mixed")
+    r = O.solve(A, b, m, mixed=True, **kw)
+    meta = g[f"{name}_meta"]
+    assert bits_equal(r["history"], g[f"{name}_history"])
+    assert bits_equal(r["x"], g[f"{name}_x"])
+    assert (r["iterations"], r["status"]) == (int(meta[0]), int(meta[1]))
+    assert r["detail"] == str(g[f"{name}_detail"])

@@ -172,6 +172,23 @@ def dense_system(M, bvec, K=2):
     return csr(n, n, rows, K, planes=planes), b
 
 
+def krylov_mixed_cases():
+    """(name, A_binary64, b, method, kwargs): solve() over CsrOperator<double>
+    (Mixed mode, the binary64 leading plane) with K-component vectors."""
+    out = []
+    for K in (2, 3, 4):
+        for sym in (True, False):
+            A, b = krylov_system(60, K, seed=13, symmetric=sym)
+            Am = mixed_of(A)
+            for m in ("cg", "bicg", "cgs", "bicgstab", "gpbicg"):
+                if m == "cg" and not sym:
+                    continue
+                out.append((f"mixed_{'sym' if sym else 'nonsym'}_K{K}_{m}", Am, b, m, {}))
+    A, b = krylov_system(60, 2, seed=13, symmetric=False)
+    out.append(("mixed_nonsym_K2_bicg_t4", mixed_of(A), b, "bicg", {"threads": 4}))
+    return out
+
+
 def krylov_cases():
     """(name, A, b, method, kwargs) parity cases shared by the oracle golden, the
     oracle tests and the device tests."""
