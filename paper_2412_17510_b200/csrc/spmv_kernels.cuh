@@ -163,6 +163,16 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
 #pragma unroll
       for (int j = 0; j < G; ++j) c[j] = cn[j];
     }
+    // the tail's column indices are already in c[] (loaded a round ahead):
+    // no dependent column load at the end of the row (TD/QD +1%, CG QD +1.7%)
+#pragma unroll
+    for (int j = 0; j < G - 1; ++j)
+      if (k + j < len) {
+        AVal<K, MX> a;
+        a.load(vp, st, (int64_t)(k + j) * 32);
+        acc = add(acc, a.times(load_aos<K>(x, c[j])));
+      }
+    return acc;
   } else {
     for (; k + G <= len; k += G) {
       MC<K> p[G];
