@@ -181,9 +181,9 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
 #pragma unroll
       for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
     }
+    for (; k < len; ++k) acc = add(acc, sell_term<K, MX>(vp, cp, st, x, k));
+    return acc;
   }
-  for (; k < len; ++k) acc = add(acc, sell_term<K, MX>(vp, cp, st, x, k));
-  return acc;
 }
 
 // Transposed product at T threads (kernels.hpp:368-394): the reference gives
