@@ -20,6 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(_HERE, "libmpsoracle.so")
 REF_SO = os.path.join(_HERE, "_ref", "libmpsref.so")
+REF_V3_SO = os.path.join(_HERE, "_ref", "libmpsref_v3.so")  # same sources, -march=x86-64-v3
 
 _P = ctypes.c_void_p
 _i64, _f64, _i32, _u64 = ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_uint64
@@ -239,10 +240,34 @@ def solve(A, b, method="bicgstab", order=LANE4, threads=1, rel_tol=1e-13, abs_to
 
 # --------------------------------------------------------------------------- real reference
 _ref = None
+_ref_path = REF_SO
 
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+def host_has_avx2_fma() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = next((l for l in f if l.startswith("flags")), "").split()
+        return "avx2" in flags and "fma" in flags
+    except OSError:
+        return False
+
+
+def use_ref_build(v3: bool) -> bool:
+    """Select the reference build later ref() calls use: the reference's own
+    flags (default) or the x86-64-v3 build.  Objects made with one build must
+    not be passed to the other.  Returns False (and keeps the default) when
+    the v3 build or an AVX2+FMA host is missing."""
+    global _ref, _ref_path
+    want = REF_V3_SO if v3 else REF_SO
+    if v3 and not (os.path.exists(REF_V3_SO) and host_has_avx2_fma()):
+        return False
+    if want != _ref_path:
+        _ref, _ref_path = None, want
+    return True
 
 
 def ref():
@@ -250,7 +275,7 @@ def ref():
     if _ref is None:
         if not ref_available():
             raise RuntimeError(f"{REF_SO} missing: run `make -C oracle ref` where /root/reference exists")
-        L = ctypes.CDLL(REF_SO)
+        L = ctypes.CDLL(_ref_path)
         L.ref_last_error.restype = ctypes.c_char_p
         L.ref_csr_create.argtypes = [_i32, _i64, _i64, _P, _P, _P]
         L.ref_csr_create.restype = _P
