@@ -155,3 +155,35 @@ def test_mixed_solve_exact_dots_bit_equal_reference(ctx, case):
     assert bits_equal(np.array(res.report.residual_history), g[f"{name}_history"])
     assert bits_equal(res.x, g[f"{name}_x"])
     assert res.report.final_true_residual == meta[3] and res.report.detail == str(g[f"{name}_detail"])
+
+
+# ---- edge cases: empty and 1x1 systems, a single iteration, x0 = exact ------------
+@pytest.mark.parametrize("m", O.METHODS)
+@pytest.mark.parametrize("exact", [True, False])
+def test_solve_edge_cases_match_oracle(ctx, m, exact):
+    from tests.util import csr, dense_system
+
+    cases = []
+    cases.append(("one", *dense_system([[3.0]], [1.5]), {}))
+    cases.append(("one_iter", *krylov_system(40, 2, seed=4, symmetric=m == "cg"), {"max_iters": 1}))
+    D, bd = dense_system(np.diag([2.0, 4.0, 8.0]), [2.0, 4.0, 8.0])
+    cases.append(("x0_exact", D, bd, {"x0": [1.0, 1.0, 1.0]}))
+    cases.append(("zero_rhs", D, np.zeros_like(bd), {}))
+    for name, A, b, kw in cases:
+        r = _run(ctx, A, b, m, exact=exact, **dict(kw))
+        ref = O.solve(A, b, m, **kw)
+        assert (r.report.iterations, int(r.report.status)) == (ref["iterations"], ref["status"]), name
+        assert r.report.detail == ref["detail"], name
+        if exact:
+            assert bits_equal(np.array(r.report.residual_history), ref["history"]), name
+            assert bits_equal(r.x, ref["x"]), name
+
+
+def test_solve_empty_system(ctx):
+    from tests.util import csr
+
+    A = csr(0, 0, [], 2)
+    b = np.zeros((0, 2))
+    for m in O.METHODS:
+        r = _run(ctx, A, b, m, exact=False)
+        assert r.report.converged and r.report.iterations == 0 and r.x.shape == (0, 2)
