@@ -48,6 +48,10 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
          *hist = nullptr, *loc = nullptr, *gath = nullptr, *pend = nullptr;
   CgState<K>* dst = nullptr;
   const int64_t max_iters = cfg->max_iters;
+  // FAST order: the iteration's vector updates and dots use the fused
+  // product-accumulate too (MPSG_CG_FUSED=0 keeps the reference's add(mul))
+  const char* efu = std::getenv("MPSG_CG_FUSED");
+  const bool fused = order == MPSG_ORDER_FAST && K > 2 && !(efu && efu[0] == '0');
   cudaGraphExec_t gexec = nullptr;
   cudaGraph_t graph = nullptr;
   auto cleanup = [&]() {
@@ -96,7 +100,11 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   auto reduce = [&](auto mode_tag, int post, const double* u, const double* v, double* xx, double* rr,
                     int gate) -> int {
     constexpr int MODE = decltype(mode_tag)::value;
-    cg_reduce_kernel<K, MODE><<<G, DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part, gate, D ? loc : nullptr);
+    if (fused)
+      cg_reduce_kernel<K, MODE, true><<<G, DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part, gate,
+                                                                  D ? loc : nullptr);
+    else
+      cg_reduce_kernel<K, MODE><<<G, DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part, gate, D ? loc : nullptr);
     if (D) {
       int e = allgather_mc(D->comm, loc, gath, K, st);
       if (e) return e;
@@ -144,7 +152,10 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
     if (e) return e;
     if ((e = reduce(Dot{}, POST_SIGMA, p, q, nullptr, nullptr, 1))) return e;
     if ((e = reduce(Upd{}, POST_RHO, p, q, x, r, 1))) return e;
-    cg_update_p_kernel<K><<<ub, 256, 0, st>>>(dst, n, r, p);
+    if (fused)
+      cg_update_p_kernel<K, true><<<ub, 256, 0, st>>>(dst, n, r, p);
+    else
+      cg_update_p_kernel<K><<<ub, 256, 0, st>>>(dst, n, r, p);
     return cudaGetLastError() == cudaSuccess ? MPSG_OK : fail(ctx, MPSG_E_CUDA, "cg: update launch failed");
   };
   int status = CG_RUNNING;

@@ -49,6 +49,16 @@ struct CgState {
   unsigned ticket;    // last-block arrival counter (self-resetting)
 };
 
+// acc + a*b: the reference's add(acc, mul(a, b)), or with the FAST order the
+// fused form with one renormalisation (mc_arith.cuh fma_fast)
+template <bool F, int K>
+MPSG_DI MC<K> pma(const MC<K>& acc, const MC<K>& a, const MC<K>& b) {
+  if constexpr (F)
+    return fma_fast(acc, a, b);
+  else
+    return add(acc, mul(a, b));
+}
+
 enum DotPost {
   POST_BNORM = 0,  // bnorm = sqrt(<b,b>); threshold; caps
   POST_R0 = 1,     // <r,r>: rho; history[0]; converged-at-start test
@@ -187,7 +197,7 @@ MPSG_DI void reduce_finish(CgState<K>* st, int post, MC<K> acc, double* partial,
 // The grid is sized to one resident wave (SMs x occupancy); each block owns a
 // contiguous segment that its threads stride through (coalesced).
 // local_out != nullptr (multi-GPU): see reduce_finish.
-template <int K, int MODE>
+template <int K, int MODE, bool F = false>
 __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n,
                                                                 const double* u, const double* v,
                                                                 double* x, double* r, double* partial,
@@ -233,7 +243,7 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
         un = load_aos<K>(u, i + DOT_THREADS);
         vn = load_aos<K>(v, i + DOT_THREADS);
       }
-      acc = add(acc, mul(uu, vv));
+      acc = pma<F>(acc, uu, vv);
     }
   } else if constexpr (MODE == 1) {
     int64_t i = lo + threadIdx.x;
@@ -252,11 +262,11 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
         xn = load_aos_rw<K>(x, i + DOT_THREADS);
         rn = load_aos_rw<K>(r, i + DOT_THREADS);
       }
-      const MC<K> xi = add(xx, mul(alpha, pp));
-      const MC<K> ri = add(rr, mul(malpha, qq));
+      const MC<K> xi = pma<F>(xx, alpha, pp);
+      const MC<K> ri = pma<F>(rr, malpha, qq);
       store_aos<K>(x, i, xi);
       store_aos<K>(r, i, ri);
-      acc = add(acc, mul(ri, ri));
+      acc = pma<F>(acc, ri, ri);
     }
   } else {
     for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) acc = add(acc, term(i));
@@ -275,14 +285,14 @@ __global__ void cg_post_gathered_kernel(CgState<K>* st, int post, const double* 
 }
 
 // p = r + beta p (krylov.hpp:272)
-template <int K>
+template <int K, bool F = false>
 __global__ void __launch_bounds__(256) cg_update_p_kernel(const CgState<K>* st, int64_t n,
                                                           const double* r, double* p) {
   if (st->status != CG_RUNNING) return;
   const MC<K> beta = st->beta;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(beta, load_aos_rw<K>(p, i))));
+    store_aos<K>(p, i, pma<F>(load_aos_rw<K>(r, i), beta, load_aos_rw<K>(p, i)));
 }
 
 // Initial state: r = b (or b - A x0 computed by the caller), p = r.

@@ -316,6 +316,53 @@ MPSG_DI MC<4> mul_d(const MC<4>& x, double y) {  // multicomp.hpp:273-277
   return renorm<4, 5>(t);
 }
 
+// FAST-mode product-accumulate acc + a*x with ONE renormalisation per
+// nonzero (SURVEY 8(a) hard part 2: "the fast mode may fuse mul+add into one
+// renormalisation per nnz, provided the componentwise bound holds"): the
+// product's five pre-normalisation terms (qd_mul_prenorm) enter the add with
+// the last two merged, skipping the product's own renorm (21 of ~206 fp64
+// operations per nonzero).  Not the reference's bits; checked against the
+// bound |y - y_ref| <= 4 rowlen u sum|a||x| in tests/test_gpu_spmv.py.
+MPSG_DI MC<4> fma_fast(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
+  double p[5];
+  qd_mul_prenorm(a.c, x.c, p);
+  const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
+  double t[5];
+  qd_add_prenorm(acc.c, pv, t);
+  return renorm<4, 5>(t);
+}
+MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
+  const double ae[4] = {a.c[0], a.c[1], a.c[2], 0.0};
+  const double xe[4] = {x.c[0], x.c[1], x.c[2], 0.0};
+  double p[5];
+  qd_mul_prenorm(ae, xe, p);
+  const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
+  const double ce[4] = {acc.c[0], acc.c[1], acc.c[2], 0.0};
+  double t[5];
+  qd_add_prenorm(ce, pv, t);
+  return renorm<3, 5>(t);
+}
+MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) { return add(acc, mul(a, x)); }
+// Mixed mode: acc + x*a with a binary64 matrix value (mul_by_double's
+// pre-normalisation terms straight into the add)
+MPSG_DI MC<4> fma_fast_d(const MC<4>& acc, const MC<4>& x, double a) {
+  double p[5];
+  qd_mul_d_prenorm(x.c, a, p);
+  const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
+  double t[5];
+  qd_add_prenorm(acc.c, pv, t);
+  return renorm<4, 5>(t);
+}
+MPSG_DI MC<3> fma_fast_d(const MC<3>& acc, const MC<3>& x, double a) {
+  double p[4];
+  td_mul_d_prenorm(x.c, a, p);
+  const double ce[4] = {acc.c[0], acc.c[1], acc.c[2], 0.0};
+  double t[5];
+  qd_add_prenorm(ce, p, t);
+  return renorm<3, 5>(t);
+}
+MPSG_DI MC<2> fma_fast_d(const MC<2>& acc, const MC<2>& x, double a) { return add(acc, mul_d(x, a)); }
+
 template <int K>
 MPSG_DI MC<K> zero() {
   MC<K> r;

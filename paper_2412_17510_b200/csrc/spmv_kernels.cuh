@@ -59,6 +59,8 @@ struct AVal<K, false> {  // Pure: K component planes, mul(a, v)
   MPSG_DI void load(const double* __restrict__ vp, int64_t st, int64_t e) { a = load_planes_stream<K>(vp, st, e); }
   MPSG_DI void load_ldg(const double* __restrict__ vp, int64_t st, int64_t e) { a = load_planes<K>(vp, st, e); }
   MPSG_DI MC<K> times(const MC<K>& v) const { return mul(a, v); }
+  // FAST order: acc + a*v with one renormalisation (mc_arith.cuh fma_fast)
+  MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_fast(acc, a, v); }
 };
 template <int K>
 struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
@@ -67,6 +69,7 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
   MPSG_DI void load(const double* __restrict__ vp, int64_t, int64_t e) { a = ld_f64_stream(vp + e); }
   MPSG_DI void load_ldg(const double* __restrict__ vp, int64_t, int64_t e) { a = __ldg(vp + e); }
   MPSG_DI MC<K> times(const MC<K>& v) const { return mul_d(v, a); }
+  MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_fast_d(acc, v, a); }
 };
 
 // ---------------------------------------------------------------------------
@@ -136,7 +139,7 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
 // then added in order.  PF = 1 also loads the next group's column indices a
 // round ahead, so its gathers issue as soon as the group starts.  DD: G = 4,
 // no prefetch (occupancy-bound); TD/QD: G = 2 with prefetch (64 registers).
-template <int K, bool MX>
+template <int K, bool MX, bool FUSED = false>
 MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
                          const double* __restrict__ x, int len) {
   constexpr int G = K == 2 ? 4 : 2;
@@ -151,15 +154,27 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
       int cn[G];
 #pragma unroll
       for (int j = 0; j < G; ++j) cn[j] = (k + G + j < len) ? ld_s32_stream(cp + (int64_t)(k + G + j) * 32) : 0;
-      MC<K> p[G];
+      if constexpr (FUSED) {
+        AVal<K, MX> a[G];
+        MC<K> v[G];
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        AVal<K, MX> a;
-        a.load(vp, st, (int64_t)(k + j) * 32);
-        p[j] = a.times(load_aos<K>(x, c[j]));
+        for (int j = 0; j < G; ++j) {
+          a[j].load(vp, st, (int64_t)(k + j) * 32);
+          v[j] = load_aos<K>(x, c[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) acc = a[j].accumulate(acc, v[j]);
+      } else {
+        MC<K> p[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          AVal<K, MX> a;
+          a.load(vp, st, (int64_t)(k + j) * 32);
+          p[j] = a.times(load_aos<K>(x, c[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
       }
-#pragma unroll
-      for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
 #pragma unroll
       for (int j = 0; j < G; ++j) c[j] = cn[j];
     }
@@ -170,7 +185,10 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
       if (k + j < len) {
         AVal<K, MX> a;
         a.load(vp, st, (int64_t)(k + j) * 32);
-        acc = add(acc, a.times(load_aos<K>(x, c[j])));
+        if constexpr (FUSED)
+          acc = a.accumulate(acc, load_aos<K>(x, c[j]));
+        else
+          acc = add(acc, a.times(load_aos<K>(x, c[j])));
       }
     return acc;
   } else {
@@ -234,6 +252,8 @@ MPSG_DI MC<K> sell_row(const SellView& S, const double* __restrict__ x, int s, i
   const double* __restrict__ vp = S.val + base;
   if constexpr (ORDER == ORDER_SCALAR)
     return scalar_row<K, MX>(vp, cp, S.stride, x, len);
+  else if constexpr (ORDER == ORDER_FAST)
+    return scalar_row<K, MX, true>(vp, cp, S.stride, x, len);  // fused multiply-accumulate (TD/QD)
   else
     return lane4_row<K, MX>(vp, cp, S.stride, x, len);
 }
@@ -335,17 +355,22 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
     }
     s1 = f1.finish();
     s2 = f2.finish();
-  } else if constexpr (ORDER == ORDER_SCALAR) {
+  } else if constexpr (ORDER == ORDER_SCALAR || ORDER == ORDER_FAST) {
     int c = len > 0 ? ld_s32_stream(cp) : 0;  // column index loaded a round ahead
     for (int k = 0; k < len; ++k) {
       const int64_t e = (int64_t)k * 16;
       const int cn = (k + 1 < len) ? ld_s32_stream(cp + e + 16) : 0;
       AVal<K, MX> a;
       a.load(vp, st, e);
-      MC<K> p1 = a.times(load_aos<K>(x1, c));
-      MC<K> p2 = a.times(load_aos<K>(x2, c));
-      s1 = add(s1, p1);
-      s2 = add(s2, p2);
+      if constexpr (ORDER == ORDER_FAST) {  // one renormalisation per product-accumulate
+        s1 = a.accumulate(s1, load_aos<K>(x1, c));
+        s2 = a.accumulate(s2, load_aos<K>(x2, c));
+      } else {
+        MC<K> p1 = a.times(load_aos<K>(x1, c));
+        MC<K> p2 = a.times(load_aos<K>(x2, c));
+        s1 = add(s1, p1);
+        s2 = add(s2, p2);
+      }
       c = cn;
     }
   } else {
@@ -496,7 +521,7 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #endif
   if constexpr (!CPLX && MX && MPSG_LONG_MX_U > 1) {
     // Mixed (8-byte values): U elements per lane per round, loads in flight
-    // together, added in the lane's element order (same bits as U = 1)
+    // together, accumulated in the lane's element order (same bits as U = 1)
     constexpr int U = MPSG_LONG_MX_U;
     for (; k + 32 * (U - 1) < e; k += 32 * U) {
       int c[U];
@@ -509,16 +534,17 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = load_aos<K>(xre, c[u]);
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[0] = add(acc[0], mul_d(v[u], a[u]));
+      for (int u = 0; u < U; ++u) acc[0] = fma_fast_d(acc[0], v[u], a[u]);
     }
-    for (; k < e; k += 32) acc[0] = add(acc[0], mul_d(load_aos<K>(xre, ld_s32_stream(L.col + k)), ld_f64_stream(L.val + k)));
+    for (; k < e; k += 32)
+      acc[0] = fma_fast_d(acc[0], load_aos<K>(xre, ld_s32_stream(L.col + k)), ld_f64_stream(L.val + k));
   } else if constexpr (!CPLX) {
     int c = k < e ? ld_s32_stream(L.col + k) : 0;
     for (; k < e; k += 32) {
       const int cn = k + 32 < e ? ld_s32_stream(L.col + k + 32) : 0;
       AVal<K, MX> a;
       a.load(L.val, L.stride, k);
-      acc[0] = add(acc[0], a.times(load_aos<K>(xre, c)));
+      acc[0] = a.accumulate(acc[0], load_aos<K>(xre, c));  // FAST: one renormalisation per nonzero
       c = cn;
     }
   } else {
@@ -528,10 +554,10 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
       are.load(L.val, L.stride, k);
       aim.load(L.val + (int64_t)AVal<K, MX>::NPL * L.stride, L.stride, k);
       MC<K> vr = load_aos<K>(xre, c), vi = load_aos<K>(xim, c);
-      acc[0] = add(acc[0], are.times(vr));
-      acc[1] = add(acc[1], aim.times(vi));
-      acc[2] = add(acc[2], are.times(vi));
-      acc[3] = add(acc[3], aim.times(vr));
+      acc[0] = are.accumulate(acc[0], vr);
+      acc[1] = aim.accumulate(acc[1], vi);
+      acc[2] = are.accumulate(acc[2], vi);
+      acc[3] = aim.accumulate(acc[3], vr);
     }
   }
 #pragma unroll
