@@ -216,13 +216,17 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
   // ------------------------------------------------------------ solver_init
   // (krylov.hpp:160-201)
   if (vb) KR_TRY(cudaMemcpyAsync(b, b_host, vb, cudaMemcpyHostToDevice, st));
-  kr_init_state_kernel<K><<<1, 1, 0, st>>>(dst, cfg->rel_tol, cfg->abs_tol, (long long)max_iters, hist, pend);
+  // FAST order with tree dots: fused product-accumulates in the vector kernels
+  // too (MPSG_KR_FUSED=0 keeps the reference's add(mul)); never with exact dots
+  const char* efu = std::getenv("MPSG_KR_FUSED");
+  const int fused = (!seq && order == MPSG_ORDER_FAST && K > 2 && !(efu && efu[0] == '0')) ? 1 : 0;
+  kr_init_state_kernel<K><<<1, 1, 0, st>>>(dst, cfg->rel_tol, cfg->abs_tol, (long long)max_iters, hist, pend, fused);
   // bnorm = norm2(b); threshold, divergence cap, breakdown floor (:185-189)
   KR_RC(L.template reduce<1>(
       GATE_ALWAYS,
-      [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
+      [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
         const MC<K> bi = load_aos_rw<K>(b, i);
-        d[0] = mul(bi, bi);
+        d[0] = KrTerm<K>{bi, bi};
       },
       [=] __device__(KrState<K> * s, MC<K> * d) {
         const MC<K> bn = sqrt_mc(d[0]);
@@ -242,11 +246,11 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
   // r0 = norm2(r); history[0]; converged-at-start test (:191-197)
   KR_RC(L.template reduce<1>(
       GATE_ALWAYS,
-      [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
+      [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
         const MC<K> bi = load_aos_rw<K>(b, i);
         const MC<K> ri = has_x0 ? sub(bi, load_aos_rw<K>(q, i)) : bi;
         store_aos<K>(r, i, ri);
-        d[0] = mul(ri, ri);
+        d[0] = KrTerm<K>{ri, ri};
       },
       [=] __device__(KrState<K> * s, MC<K> * d) {
         const MC<K> rn = sqrt_mc(d[0]);
@@ -264,13 +268,13 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
   const bool is_cg = method == MPSG_CG;
   KR_RC(L.template reduce<1>(
       GATE_RUN,
-      [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
+      [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
         const MC<K> ri = load_aos_rw<K>(r, i);
         store_aos<K>(p, i, ri);
         if (rt) store_aos<K>(rt, i, ri);
         if (pt) store_aos<K>(pt, i, ri);
         if (method == MPSG_CGS) store_aos<K>(u, i, ri);
-        d[0] = mul(ri, ri);
+        d[0] = KrTerm<K>{ri, ri};
       },
       [=] __device__(KrState<K> * s, MC<K> * d) {
         s->sc.rho = d[0];
@@ -305,19 +309,19 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         if ((e = apply(p, q))) return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
-                   d[0] = mul(load_aos_rw<K>(p, i), load_aos_rw<K>(q, i));  // sigma = <p, q>
+                 [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
+                   d[0] = KrTerm<K>{load_aos_rw<K>(p, i), load_aos_rw<K>(q, i)};  // sigma = <p, q>
                  },
                  post_alpha)))
           return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
-                   const MC<K> xi = add(load_aos_rw<K>(x, i), mul(c.alpha, load_aos_rw<K>(p, i)));
-                   const MC<K> ri = add(load_aos_rw<K>(r, i), mul(negate(c.alpha), load_aos_rw<K>(q, i)));
+                 [=] __device__(const KrScalars<K>& c, int64_t i, KrTerm<K>* d) {
+                   const MC<K> xi = pma(c, load_aos_rw<K>(x, i), c.alpha, load_aos_rw<K>(p, i));
+                   const MC<K> ri = pma(c, load_aos_rw<K>(r, i), negate(c.alpha), load_aos_rw<K>(q, i));
                    store_aos<K>(x, i, xi);
                    store_aos<K>(r, i, ri);
-                   d[0] = mul(ri, ri);  // rho' = <r, r>
+                   d[0] = KrTerm<K>{ri, ri};  // rho' = <r, r>
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) {
                    if (!kr_record(s, d[0])) return;
@@ -327,7 +331,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                  })))
           return e;
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
-          store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, load_aos_rw<K>(p, i))));
+          store_aos<K>(p, i, pma(c, load_aos_rw<K>(r, i), c.beta, load_aos_rw<K>(p, i)));
         });
 
       case MPSG_BICG:  // krylov.hpp:293-330
@@ -335,37 +339,37 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         if ((e = apply_t(pt, qt))) return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
-                   d[0] = mul(load_aos_rw<K>(pt, i), load_aos_rw<K>(q, i));  // sigma = <p~, q>
+                 [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
+                   d[0] = KrTerm<K>{load_aos_rw<K>(pt, i), load_aos_rw<K>(q, i)};  // sigma = <p~, q>
                  },
                  post_alpha)))
           return e;
         if ((e = L.template reduce<2>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
+                 [=] __device__(const KrScalars<K>& c, int64_t i, KrTerm<K>* d) {
                    const MC<K> ma = negate(c.alpha);
-                   const MC<K> xi = add(load_aos_rw<K>(x, i), mul(c.alpha, load_aos_rw<K>(p, i)));
-                   const MC<K> ri = add(load_aos_rw<K>(r, i), mul(ma, load_aos_rw<K>(q, i)));
-                   const MC<K> rti = add(load_aos_rw<K>(rt, i), mul(ma, load_aos_rw<K>(qt, i)));
+                   const MC<K> xi = pma(c, load_aos_rw<K>(x, i), c.alpha, load_aos_rw<K>(p, i));
+                   const MC<K> ri = pma(c, load_aos_rw<K>(r, i), ma, load_aos_rw<K>(q, i));
+                   const MC<K> rti = pma(c, load_aos_rw<K>(rt, i), ma, load_aos_rw<K>(qt, i));
                    store_aos<K>(x, i, xi);
                    store_aos<K>(r, i, ri);
                    store_aos<K>(rt, i, rti);
-                   d[0] = mul(ri, ri);   // ||r||^2
-                   d[1] = mul(rti, ri);  // rho' = <r~, r>
+                   d[0] = KrTerm<K>{ri, ri};   // ||r||^2
+                   d[1] = KrTerm<K>{rti, ri};  // rho' = <r~, r>
                  },
                  post_rho_next)))
           return e;
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
-          store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, load_aos_rw<K>(p, i))));
-          store_aos<K>(pt, i, add(load_aos_rw<K>(rt, i), mul(c.beta, load_aos_rw<K>(pt, i))));
+          store_aos<K>(p, i, pma(c, load_aos_rw<K>(r, i), c.beta, load_aos_rw<K>(p, i)));
+          store_aos<K>(pt, i, pma(c, load_aos_rw<K>(rt, i), c.beta, load_aos_rw<K>(pt, i)));
         });
 
       case MPSG_CGS:  // krylov.hpp:350-389
         if ((e = apply(p, v))) return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
-                   d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i));  // sigma = <r~, v>
+                 [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
+                   d[0] = KrTerm<K>{load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i)};  // sigma = <r~, v>
                  },
                  post_alpha)))
           return e;
@@ -376,26 +380,26 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                const MC<K> ti = add(ui, qi);
                store_aos<K>(q, i, qi);
                store_aos<K>(t, i, ti);
-               store_aos<K>(x, i, add(load_aos_rw<K>(x, i), mul(c.alpha, ti)));
+               store_aos<K>(x, i, pma(c, load_aos_rw<K>(x, i), c.alpha, ti));
              })))
           return e;
         if ((e = apply(t, w))) return e;
         if ((e = L.template reduce<2>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
-                   const MC<K> ri = add(load_aos_rw<K>(r, i), mul(negate(c.alpha), load_aos_rw<K>(w, i)));
+                 [=] __device__(const KrScalars<K>& c, int64_t i, KrTerm<K>* d) {
+                   const MC<K> ri = pma(c, load_aos_rw<K>(r, i), negate(c.alpha), load_aos_rw<K>(w, i));
                    store_aos<K>(r, i, ri);
-                   d[0] = mul(ri, ri);
-                   d[1] = mul(load_aos_rw<K>(rt, i), ri);
+                   d[0] = KrTerm<K>{ri, ri};
+                   d[1] = KrTerm<K>{load_aos_rw<K>(rt, i), ri};
                  },
                  post_rho_next)))
           return e;
         // u = r + beta q; p = u + beta (q + beta p)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           const MC<K> qi = load_aos_rw<K>(q, i);
-          const MC<K> ui = add(load_aos_rw<K>(r, i), mul(c.beta, qi));
+          const MC<K> ui = pma(c, load_aos_rw<K>(r, i), c.beta, qi);
           store_aos<K>(u, i, ui);
-          store_aos<K>(p, i, add(ui, mul(c.beta, add(qi, mul(c.beta, load_aos_rw<K>(p, i))))));
+          store_aos<K>(p, i, pma(c, ui, c.beta, pma(c, qi, c.beta, load_aos_rw<K>(p, i))));
         });
 
       case MPSG_BICGSTAB: {  // krylov.hpp:407-469; s lives in q
@@ -403,18 +407,18 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         if ((e = apply(p, v))) return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
-                   d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i));  // sigma = <r~, v>
+                 [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
+                   d[0] = KrTerm<K>{load_aos_rw<K>(rt, i), load_aos_rw<K>(v, i)};  // sigma = <r~, v>
                  },
                  post_alpha)))
           return e;
         // s = r - alpha v; half-step test on ||s|| (:421-433)
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
-                   const MC<K> si = add(load_aos_rw<K>(r, i), mul(negate(c.alpha), load_aos_rw<K>(v, i)));
+                 [=] __device__(const KrScalars<K>& c, int64_t i, KrTerm<K>* d) {
+                   const MC<K> si = pma(c, load_aos_rw<K>(r, i), negate(c.alpha), load_aos_rw<K>(v, i));
                    store_aos<K>(s_, i, si);
-                   d[0] = mul(si, si);
+                   d[0] = KrTerm<K>{si, si};
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); })))
           return e;
@@ -422,10 +426,10 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         // tt = <t, t>; omega = <t, s> / tt (:434-446)
         if ((e = L.template reduce<2>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
+                 [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
                    const MC<K> ti = load_aos_rw<K>(t, i);
-                   d[0] = mul(ti, ti);
-                   d[1] = mul(ti, load_aos_rw<K>(s_, i));
+                   d[0] = KrTerm<K>{ti, ti};
+                   d[1] = KrTerm<K>{ti, load_aos_rw<K>(s_, i)};
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) {
                    if (kr_tiny(to_double(d[0]), s->floor)) {
@@ -440,18 +444,18 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         // x += alpha p (+ omega s); r = s (- omega t); ||r||, <r~, r> (:426-427, 447-451)
         if ((e = L.template reduce<2>(
                  GATE_RUN_HALF,
-                 [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
+                 [=] __device__(const KrScalars<K>& c, int64_t i, KrTerm<K>* d) {
                    const MC<K> si = load_aos_rw<K>(s_, i);
-                   MC<K> xi = add(load_aos_rw<K>(x, i), mul(c.alpha, load_aos_rw<K>(p, i)));
+                   MC<K> xi = pma(c, load_aos_rw<K>(x, i), c.alpha, load_aos_rw<K>(p, i));
                    MC<K> ri = si;
                    if (!c.half) {
-                     xi = add(xi, mul(c.omega, si));
-                     ri = add(si, mul(negate(c.omega), load_aos_rw<K>(t, i)));
+                     xi = pma(c, xi, c.omega, si);
+                     ri = pma(c, si, negate(c.omega), load_aos_rw<K>(t, i));
                    }
                    store_aos<K>(x, i, xi);
                    store_aos<K>(r, i, ri);
-                   d[0] = mul(ri, ri);
-                   d[1] = mul(load_aos_rw<K>(rt, i), ri);
+                   d[0] = KrTerm<K>{ri, ri};
+                   d[1] = KrTerm<K>{load_aos_rw<K>(rt, i), ri};
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) {
                    if (s->status == KR_HALF) {
@@ -468,7 +472,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         // p = r + beta (p - omega v) (:466-467)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
           const MC<K> pv = sub(load_aos_rw<K>(p, i), mul(c.omega, load_aos_rw<K>(v, i)));
-          store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, pv)));
+          store_aos<K>(p, i, pma(c, load_aos_rw<K>(r, i), c.beta, pv));
         });
       }
 
@@ -477,22 +481,22 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         if ((e = apply(p, ap))) return e;
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
-                   d[0] = mul(load_aos_rw<K>(rt, i), load_aos_rw<K>(ap, i));  // sigma = <r~, Ap>
+                 [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
+                   d[0] = KrTerm<K>{load_aos_rw<K>(rt, i), load_aos_rw<K>(ap, i)};  // sigma = <r~, Ap>
                  },
                  post_alpha)))
           return e;
         // d = t_prev - r; y = d + alpha (Ap - w); t = r - alpha Ap; half-step test (:507-522)
         if ((e = L.template reduce<1>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
+                 [=] __device__(const KrScalars<K>& c, int64_t i, KrTerm<K>* d) {
                    const MC<K> ri = load_aos_rw<K>(r, i), api = load_aos_rw<K>(ap, i);
                    const MC<K> di = sub(load_aos_rw<K>(t, i), ri);
                    store_aos<K>(dv, i, di);
-                   store_aos<K>(y, i, add(di, mul(c.alpha, sub(api, load_aos_rw<K>(w, i)))));
-                   const MC<K> ti = add(ri, mul(negate(c.alpha), api));
+                   store_aos<K>(y, i, pma(c, di, c.alpha, sub(api, load_aos_rw<K>(w, i))));
+                   const MC<K> ti = pma(c, ri, negate(c.alpha), api);
                    store_aos<K>(t, i, ti);
-                   d[0] = mul(ti, ti);
+                   d[0] = KrTerm<K>{ti, ti};
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) { kr_half_test(s, d[0]); })))
           return e;
@@ -500,13 +504,13 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         // <At, t>, <At, At>, <y, y>, <y, At>, <y, t>; zeta, eta (:523-548)
         if ((e = L.template reduce<5>(
                  GATE_RUN,
-                 [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
+                 [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
                    const MC<K> ati = load_aos_rw<K>(at, i), ti = load_aos_rw<K>(t, i), yi = load_aos_rw<K>(y, i);
-                   d[0] = mul(ati, ti);
-                   d[1] = mul(ati, ati);
-                   d[2] = mul(yi, yi);
-                   d[3] = mul(yi, ati);
-                   d[4] = mul(yi, ti);
+                   d[0] = KrTerm<K>{ati, ti};
+                   d[1] = KrTerm<K>{ati, ati};
+                   d[2] = KrTerm<K>{yi, yi};
+                   d[3] = KrTerm<K>{yi, ati};
+                   d[4] = KrTerm<K>{yi, ti};
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) {
                    const MC<K> &att = d[0], &ata = d[1], &yy = d[2], &yat = d[3], &yt = d[4];
@@ -531,25 +535,24 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         // u, z, x, r; ||r||, <r~, r> (:549-562); half step: x += alpha p, r = t
         if ((e = L.template reduce<2>(
                  GATE_RUN_HALF,
-                 [=] __device__(const KrScalars<K>& c, int64_t i, MC<K>* d) {
+                 [=] __device__(const KrScalars<K>& c, int64_t i, KrTerm<K>* d) {
                    const MC<K> ti = load_aos_rw<K>(t, i);
-                   MC<K> xi = add(load_aos_rw<K>(x, i), mul(c.alpha, load_aos_rw<K>(p, i)));
+                   MC<K> xi = pma(c, load_aos_rw<K>(x, i), c.alpha, load_aos_rw<K>(p, i));
                    MC<K> rn = ti;
                    if (!c.half) {
                      const MC<K> ri = load_aos_rw<K>(r, i);
                      const MC<K> ui = add(mul(c.zeta, load_aos_rw<K>(ap, i)),
-                                          mul(c.eta, add(load_aos_rw<K>(dv, i), mul(c.beta, load_aos_rw<K>(u, i)))));
+                                          mul(c.eta, pma(c, load_aos_rw<K>(dv, i), c.beta, load_aos_rw<K>(u, i))));
                      const MC<K> zi = sub(add(mul(c.zeta, ri), mul(c.eta, load_aos_rw<K>(z, i))), mul(c.alpha, ui));
                      store_aos<K>(u, i, ui);
                      store_aos<K>(z, i, zi);
                      xi = add(xi, zi);
-                     rn = add(add(ti, mul(negate(c.eta), load_aos_rw<K>(y, i))),
-                              mul(negate(c.zeta), load_aos_rw<K>(at, i)));
+                     rn = pma(c, pma(c, ti, negate(c.eta), load_aos_rw<K>(y, i)), negate(c.zeta), load_aos_rw<K>(at, i));
                    }
                    store_aos<K>(x, i, xi);
                    store_aos<K>(r, i, rn);
-                   d[0] = mul(rn, rn);
-                   d[1] = mul(load_aos_rw<K>(rt, i), rn);
+                   d[0] = KrTerm<K>{rn, rn};
+                   d[1] = KrTerm<K>{load_aos_rw<K>(rt, i), rn};
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) {
                    if (s->status == KR_HALF) {
@@ -568,8 +571,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
           return e;
         // w = At + beta Ap; p = r + beta (p - u); t_prev = t (already in t) (:581-585)
         return L.map(GATE_RUN, [=] __device__(const KrScalars<K>& c, int64_t i) {
-          store_aos<K>(w, i, add(load_aos_rw<K>(at, i), mul(c.beta, load_aos_rw<K>(ap, i))));
-          store_aos<K>(p, i, add(load_aos_rw<K>(r, i), mul(c.beta, sub(load_aos_rw<K>(p, i), load_aos_rw<K>(u, i)))));
+          store_aos<K>(w, i, pma(c, load_aos_rw<K>(at, i), c.beta, load_aos_rw<K>(ap, i)));
+          store_aos<K>(p, i, pma(c, load_aos_rw<K>(r, i), c.beta, sub(load_aos_rw<K>(p, i), load_aos_rw<K>(u, i))));
         });
       }
     }
@@ -633,9 +636,9 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
   KR_RC(apply(x, q));
   KR_RC(L.template reduce<1>(
       GATE_ALWAYS,
-      [=] __device__(const KrScalars<K>&, int64_t i, MC<K>* d) {
+      [=] __device__(const KrScalars<K>&, int64_t i, KrTerm<K>* d) {
         const MC<K> wi = sub(load_aos_rw<K>(b, i), load_aos_rw<K>(q, i));
-        d[0] = mul(wi, wi);
+        d[0] = KrTerm<K>{wi, wi};
       },
       [=] __device__(KrState<K> * s, MC<K> * d) { s->true_residual = to_double(sqrt_mc(d[0])); }));
   double true_res = 0.0;

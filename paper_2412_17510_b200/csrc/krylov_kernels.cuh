@@ -36,8 +36,22 @@ enum KrGate { GATE_ALWAYS = 0, GATE_RUN = 1, GATE_RUN_HALF = 2 };
 template <int K>
 struct KrScalars {
   MC<K> rho, alpha, beta, omega, zeta, eta;
-  int half;  // the half step converged (status KR_HALF)
+  int half;   // the half step converged (status KR_HALF)
+  int fused;  // FAST order with tree dots: product-accumulates with one renormalisation (fma_fast)
 };
+
+// One product term of a fused dot: the reduction adds a*b to its accumulator.
+template <int K>
+struct KrTerm {
+  MC<K> a, b;
+};
+
+// x + a*b in the bodies: the reference's add(x, mul(a, b)), or fma_fast when
+// the solve runs fused (never with the sequential, reference-exact dots).
+template <int K>
+MPSG_DI MC<K> pma(const KrScalars<K>& c, const MC<K>& x, const MC<K>& a, const MC<K>& b) {
+  return c.fused ? fma_fast(x, a, b) : add(x, mul(a, b));
+}
 
 // Reason codes of a Breakdown (the detail text after "<method>: "), shared
 // with the oracle (oracle/mpsoracle.c):
@@ -200,10 +214,10 @@ __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, i
 #pragma unroll
   for (int m = 0; m < M; ++m) acc[m] = zero<K>();
   for (int64_t i = lo + threadIdx.x; i < hi; i += KR_THREADS) {
-    MC<K> t[M];
+    KrTerm<K> t[M];
     body(sc, i, t);
 #pragma unroll
-    for (int m = 0; m < M; ++m) acc[m] = add(acc[m], t[m]);
+    for (int m = 0; m < M; ++m) acc[m] = pma(sc, acc[m], t[m].a, t[m].b);
   }
   block_reduce_m<K, M>(acc, sh);
   if (threadIdx.x == 0) {
@@ -255,10 +269,10 @@ __global__ void kr_reduce_seq_kernel(KrState<K>* st, int gate, int64_t n, Body b
 #pragma unroll
   for (int m = 0; m < M; ++m) acc[m] = zero<K>();
   for (int64_t i = 0; i < n; ++i) {
-    MC<K> t[M];
+    KrTerm<K> t[M];
     body(sc, i, t);
 #pragma unroll
-    for (int m = 0; m < M; ++m) acc[m] = add(acc[m], t[m]);
+    for (int m = 0; m < M; ++m) acc[m] = add(acc[m], mul(t[m].a, t[m].b));  // acc + u[i]*v[i] (krylov.hpp:126)
   }
   if (local_out) {
 #pragma unroll
@@ -295,9 +309,10 @@ __global__ void __launch_bounds__(256) kr_map_kernel(const KrState<K>* st, int g
 
 template <int K>
 __global__ void kr_init_state_kernel(KrState<K>* st, double rel_tol, double abs_tol, long long max_iters,
-                                     double* history, double* pend) {
+                                     double* history, double* pend, int fused) {
   st->sc.rho = st->sc.alpha = st->sc.beta = st->sc.omega = st->sc.zeta = st->sc.eta = zero<K>();
   st->sc.half = 0;
+  st->sc.fused = fused;
   st->thr = zero<K>();
   st->status = KR_RUNNING;
   st->reason = 0;

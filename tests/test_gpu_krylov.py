@@ -59,11 +59,13 @@ def test_solve_exact_dots_bit_equal_reference(ctx, case):
     assert rep.final_recurrence_residual == rep.residual_history[-1] or np.isnan(rep.final_recurrence_residual)
 
 
+@pytest.mark.parametrize("order", [M.ORDER_LANE4, M.ORDER_FAST], ids=["lane4", "fast"])
 @pytest.mark.parametrize("case", _KCASES, ids=[c[0] for c in _KCASES])
-def test_solve_tree_dots_tracks_reference(ctx, case):
+def test_solve_tree_dots_tracks_reference(ctx, case, order):
+    """order FAST also runs the fused product-accumulates (TD/QD)."""
     name, A, b, m, kw = case
     g = golden("krylov_small")
-    res = _run(ctx, A, b, m, exact=False, **dict(kw))
+    res = _run(ctx, A, b, m, exact=False, order=order, **dict(kw))
     rep = res.report
     meta = g[f"{name}_meta"]
     ref_iters, ref_status = int(meta[0]), int(meta[1])
