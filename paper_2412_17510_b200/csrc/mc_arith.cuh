@@ -342,7 +342,25 @@ MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   qd_add_prenorm(ce, pv, t);
   return renorm<3, 5>(t);
 }
-MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) { return add(acc, mul(a, x)); }
+#ifndef MPSG_DD_FUSED
+#define MPSG_DD_FUSED 1
+#endif
+MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) {
+#if MPSG_DD_FUSED
+  // the product's (p1, p2) without its quick_two_sum, straight into the add
+  double p1, p2;
+  two_prod(a.c[0], x.c[0], p1, p2);
+  p2 = dadd(p2, dadd(dmul(a.c[0], x.c[1]), dmul(a.c[1], x.c[0])));
+  double s, e;
+  two_sum(acc.c[0], p1, s, e);
+  e = dadd(e, dadd(acc.c[1], p2));
+  MC<2> r;
+  qts(s, e, r.c[0], r.c[1]);
+  return r;
+#else
+  return add(acc, mul(a, x));
+#endif
+}
 // Mixed mode: acc + x*a with a binary64 matrix value (mul_by_double's
 // pre-normalisation terms straight into the add)
 MPSG_DI MC<4> fma_fast_d(const MC<4>& acc, const MC<4>& x, double a) {
