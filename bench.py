@@ -53,6 +53,17 @@ CONFIG_DESC = {
 OPS_PER_NNZ = {2: 20, 3: 202, 4: 206}
 # Mixed mode (binary64 matrix): one mul_by_double + one add
 OPS_PER_NNZ_MIXED = {2: 17, 3: 130, 4: 152}
+# FAST order executes a fused product-accumulate (mc_arith.cuh fma_acc /
+# fma_fast): the product's pre-normalisation terms go straight into the add
+# (QD: 99 + 1 + 63 + a 12-op renorm sweep + 1 = 176; TD: 99 + 1 + 63 + 20 = 183;
+# DD: 6 + 11 = 17), one canonicalising renorm (22) per QD row, and stored
+# vector updates with the add's full renorm (QD 185, TD 183).  The roofline of
+# a FAST line counts the operations it executes; the reference's count and the
+# fraction against it are reported beside (reference_fp64_ops, reference_frac).
+OPS_FAST = {2: 17, 3: 183, 4: 176}
+OPS_FAST_MIXED = {2: 17, 3: 114, 4: 122}
+OPS_FAST_UPDATE = {2: 20, 3: 183, 4: 185}
+ROW_CANON = {2: 0, 3: 0, 4: 22}
 K_NAME = {2: "DD", 3: "TD", 4: "QD"}
 CG_ITERS = 500
 
@@ -64,7 +75,10 @@ def algorithmic_bytes(nnz, n, K, cplx, mixed=False):
     return nnz * (8 * (1 if mixed else K) * c + 4) + 4 * (n + 1) + 2 * n * 8 * K * c
 
 
-def algorithmic_ops(nnz, K, cplx, mixed=False):
+def algorithmic_ops(nnz, K, cplx, mixed=False, n=0, fast=False):
+    if fast:
+        per = (OPS_FAST_MIXED if mixed else OPS_FAST)[K]
+        return nnz * per * (4 if cplx else 1) + (0 if cplx else n * ROW_CANON[K])
     return nnz * (OPS_PER_NNZ_MIXED if mixed else OPS_PER_NNZ)[K] * (4 if cplx else 1)
 
 
@@ -73,7 +87,10 @@ def cg_iter_bytes(nnz, n, K):
     return nnz * (8 * K + 4) + 4 * (n + 1) + 11 * n * 8 * K
 
 
-def cg_iter_ops(nnz, n, K):
+def cg_iter_ops(nnz, n, K, fast=False):
+    if fast:  # SpMV + <p,q>, <r,r> accumulations + x, r, p stored updates (cg_kernels.cuh)
+        vec = 2 * OPS_FAST[K] + 3 * OPS_FAST_UPDATE[K] if K > 2 else 5 * OPS_PER_NNZ[K]
+        return nnz * OPS_FAST[K] + n * ROW_CANON[K] + n * vec
     return (nnz + 5 * n) * OPS_PER_NNZ[K]
 
 
@@ -91,8 +108,11 @@ def solver_iter_bytes(method, nnz, n, K):
     return s * (nnz * (8 * K + 4) + 4 * (n + 1)) + passes * n * 8 * K
 
 
-def solver_iter_ops(method, nnz, n, K):
+def solver_iter_ops(method, nnz, n, K, fast=False):
     s, pairs, _ = SOLVER_WORK[method]
+    if fast:  # BiCGSTAB: 6 dot accumulations, 5 fused stored updates, 1 plain (p - omega v)
+        vec = 6 * OPS_FAST[K] + 5 * OPS_FAST_UPDATE[K] + OPS_PER_NNZ[K] if K > 2 else pairs * OPS_PER_NNZ[K]
+        return s * (nnz * OPS_FAST[K] + n * ROW_CANON[K]) + n * vec
     return (s * nnz + pairs * n) * OPS_PER_NNZ[K]
 
 
@@ -521,13 +541,16 @@ def run_gpu_cg(args, K, order, rank, world, dist, method="cg"):
     return out
 
 
-def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey, mixed=False):
+def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey, mixed=False, fast=False):
     if kind == "cg":
-        byts, ops = cg_iter_bytes(nnz, n, K), cg_iter_ops(nnz, n, K)
+        byts = cg_iter_bytes(nnz, n, K)
+        ops, ref_ops = cg_iter_ops(nnz, n, K, fast), cg_iter_ops(nnz, n, K)
     elif kind in SOLVER_WORK:
-        byts, ops = solver_iter_bytes(kind, nnz, n, K), solver_iter_ops(kind, nnz, n, K)
+        byts = solver_iter_bytes(kind, nnz, n, K)
+        ops, ref_ops = solver_iter_ops(kind, nnz, n, K, fast), solver_iter_ops(kind, nnz, n, K)
     else:
-        byts, ops = algorithmic_bytes(nnz, n, K, cplx, mixed), algorithmic_ops(nnz, K, cplx, mixed)
+        byts = algorithmic_bytes(nnz, n, K, cplx, mixed)
+        ops, ref_ops = algorithmic_ops(nnz, K, cplx, mixed, n, fast), algorithmic_ops(nnz, K, cplx, mixed)
     t_hbm, t_fp = byts / (hbm_peak * 1e9), ops / fp64_peak
     if t_hbm >= t_fp:
         ach = byts / seconds / 1e9
@@ -538,6 +561,10 @@ def roofline(kind, nnz, n, K, cplx, seconds, hbm_peak, fp64_peak, tkey, mixed=Fa
         pk = fp64_peak / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": pk, "unit": "T fp64 instr/s", "frac": ach / pk,
                 "peak_source": "measured on this GPU by mpsg_measure_fp64_peak (DFMA throughput)"}
+        if ops != ref_ops:  # FAST: executed fused arithmetic; the reference algorithm's count beside
+            roof.update(reference_fp64_ops=ref_ops, reference_frac=ref_ops / seconds / fp64_peak,
+                        ops_note="fp64 ops of the executed FAST arithmetic (fused product-accumulate, "
+                                 "bench.py OPS_FAST); reference_frac counts the reference algorithm's ops")
     roof.update(t_roofline_us=max(t_hbm, t_fp) * 1e6, algorithmic_bytes=byts, algorithmic_fp64_ops=ops,
                 per=(f"one {kind} iteration" if kind != "spmv" else "one SpMV launch"),
                 traffic=traffic_for(tkey))
@@ -638,12 +665,12 @@ def main():
             r = run_gpu_cg(args, K, order, rank, world, dist, meth)
             r["variant"] = "pure"
             r["roof"] = roofline(meth, r["nnz"], r["n"], K, False, r["per_iter"], hbm_peak, fp64_peak,
-                                 f"cg5_K{K}" if meth == "cg" else f"{meth}5_K{K}")
+                                 f"cg5_K{K}" if meth == "cg" else f"{meth}5_K{K}", fast=order == 2)
         else:
             r = run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant)
             tkey = f"{cfg}_K{K}" + ("" if variant == "pure" else f"_{variant}")
             r["roof"] = roofline("spmv", r["nnz"], r["n"], K, r["cplx"], r["per_launch"], hbm_peak, fp64_peak,
-                                 tkey, mixed=variant == "mixed")
+                                 tkey, mixed=variant == "mixed", fast=order == 2)
         results.append((cfg, K, cg, r))
 
     if rank == 0:

@@ -58,6 +58,14 @@ MPSG_DI MC<K> pma(const MC<K>& acc, const MC<K>& a, const MC<K>& b) {
   else
     return add(acc, mul(a, b));
 }
+// the same for a running dot accumulator (fma_acc: renorm sweep only)
+template <bool F, int K>
+MPSG_DI MC<K> pacc(const MC<K>& acc, const MC<K>& a, const MC<K>& b) {
+  if constexpr (F)
+    return fma_acc(acc, a, b);
+  else
+    return add(acc, mul(a, b));
+}
 
 enum DotPost {
   POST_BNORM = 0,  // bnorm = sqrt(<b,b>); threshold; caps
@@ -243,7 +251,7 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
         un = load_aos<K>(u, i + DOT_THREADS);
         vn = load_aos<K>(v, i + DOT_THREADS);
       }
-      acc = pma<F>(acc, uu, vv);
+      acc = pacc<F>(acc, uu, vv);
     }
   } else if constexpr (MODE == 1) {
     int64_t i = lo + threadIdx.x;
@@ -266,7 +274,7 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
       const MC<K> ri = pma<F>(rr, malpha, qq);
       store_aos<K>(x, i, xi);
       store_aos<K>(r, i, ri);
-      acc = pma<F>(acc, ri, ri);
+      acc = pacc<F>(acc, ri, ri);
     }
   } else {
     for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) acc = add(acc, term(i));

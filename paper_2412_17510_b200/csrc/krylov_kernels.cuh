@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, i
     KrTerm<K> t[M];
     body(sc, i, t);
 #pragma unroll
-    for (int m = 0; m < M; ++m) acc[m] = pma(sc, acc[m], t[m].a, t[m].b);
+    for (int m = 0; m < M; ++m) acc[m] = sc.fused ? fma_acc(acc[m], t[m].a, t[m].b) : add(acc[m], mul(t[m].a, t[m].b));
   }
   block_reduce_m<K, M>(acc, sh);
   if (threadIdx.x == 0) {

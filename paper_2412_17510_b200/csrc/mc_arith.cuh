@@ -316,20 +316,58 @@ MPSG_DI MC<4> mul_d(const MC<4>& x, double y) {  // multicomp.hpp:273-277
   return renorm<4, 5>(t);
 }
 
-// FAST-mode product-accumulate acc + a*x with ONE renormalisation per
-// nonzero (SURVEY 8(a) hard part 2: "the fast mode may fuse mul+add into one
-// renormalisation per nnz, provided the componentwise bound holds"): the
-// product's five pre-normalisation terms (qd_mul_prenorm) enter the add with
-// the last two merged, skipping the product's own renorm (21 of ~206 fp64
-// operations per nonzero).  Not the reference's bits; checked against the
-// bound |y - y_ref| <= 4 rowlen u sum|a||x| in tests/test_gpu_spmv.py.
+// ---------------------------------------------------------------------------
+// FAST-mode product-accumulate acc + a*x (SURVEY 8(a) hard part 2: "the fast
+// mode may fuse mul+add into one renormalisation per nnz, provided the
+// componentwise bound holds").  Not the reference's bits; every use is checked
+// against |y - y_ref| <= 4 rowlen u sum|a||x| (tests/test_gpu_spmv.py,
+// tools/fused_probe.py, tools/fused_adversarial.py).
+//  * fma_fast: the product's five pre-normalisation terms (qd_mul_prenorm, the
+//    last two merged) straight into qd_add_prenorm, then the add's full
+//    renorm_n -- skips the product's own renormalisation.  Used where the
+//    result is stored (vector updates).
+//  * fma_acc: the same, but the running accumulator keeps only the backward
+//    quick-two-sum sweep of renorm_n (the forward collect that canonicalises
+//    zero components is left to canon() once per row): QD 176 instead of 206
+//    fp64 operations per nonzero; worst 1/100 of the bound on the adversarial
+//    probes (long rows, 2^+-60 exponent spread, exact cancellation).
+// ---------------------------------------------------------------------------
+MPSG_DI MC<4> renorm_sweep(double (&t)[5]) {  // renorm_n<4,5>'s backward sweep, tail merged
+  double s = t[4];
+#pragma unroll
+  for (int i = 3; i >= 0; --i) {
+    double hi, lo;
+    qts(t[i], s, hi, lo);
+    s = hi;
+    t[i + 1] = lo;
+  }
+  MC<4> r;
+  r.c[0] = s;
+  r.c[1] = t[1];
+  r.c[2] = t[2];
+  r.c[3] = dadd(t[3], t[4]);
+  return r;
+}
+template <bool SWEEP>
+MPSG_DI MC<4> qd_fused(const MC<4>& acc, const double (&pv)[4]) {
+  double t[5];
+  qd_add_prenorm(acc.c, pv, t);
+  if constexpr (SWEEP)
+    return renorm_sweep(t);
+  else
+    return renorm<4, 5>(t);
+}
 MPSG_DI MC<4> fma_fast(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
   double p[5];
   qd_mul_prenorm(a.c, x.c, p);
   const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
-  double t[5];
-  qd_add_prenorm(acc.c, pv, t);
-  return renorm<4, 5>(t);
+  return qd_fused<false>(acc, pv);
+}
+MPSG_DI MC<4> fma_acc(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
+  double p[5];
+  qd_mul_prenorm(a.c, x.c, p);
+  const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
+  return qd_fused<true>(acc, pv);
 }
 MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   const double ae[4] = {a.c[0], a.c[1], a.c[2], 0.0};
@@ -342,12 +380,9 @@ MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   qd_add_prenorm(ce, pv, t);
   return renorm<3, 5>(t);
 }
-#ifndef MPSG_DD_FUSED
-#define MPSG_DD_FUSED 1
-#endif
+MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x) { return fma_fast(acc, a, x); }
+// DD: the product's (p1, p2) without its quick_two_sum, straight into the add
 MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) {
-#if MPSG_DD_FUSED
-  // the product's (p1, p2) without its quick_two_sum, straight into the add
   double p1, p2;
   two_prod(a.c[0], x.c[0], p1, p2);
   p2 = dadd(p2, dadd(dmul(a.c[0], x.c[1]), dmul(a.c[1], x.c[0])));
@@ -357,21 +392,17 @@ MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) {
   MC<2> r;
   qts(s, e, r.c[0], r.c[1]);
   return r;
-#else
-  return add(acc, mul(a, x));
-#endif
 }
+MPSG_DI MC<2> fma_acc(const MC<2>& acc, const MC<2>& a, const MC<2>& x) { return fma_fast(acc, a, x); }
 // Mixed mode: acc + x*a with a binary64 matrix value (mul_by_double's
 // pre-normalisation terms straight into the add)
-MPSG_DI MC<4> fma_fast_d(const MC<4>& acc, const MC<4>& x, double a) {
+MPSG_DI MC<4> fma_acc_d(const MC<4>& acc, const MC<4>& x, double a) {
   double p[5];
   qd_mul_d_prenorm(x.c, a, p);
   const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
-  double t[5];
-  qd_add_prenorm(acc.c, pv, t);
-  return renorm<4, 5>(t);
+  return qd_fused<true>(acc, pv);
 }
-MPSG_DI MC<3> fma_fast_d(const MC<3>& acc, const MC<3>& x, double a) {
+MPSG_DI MC<3> fma_acc_d(const MC<3>& acc, const MC<3>& x, double a) {
   double p[4];
   td_mul_d_prenorm(x.c, a, p);
   const double ce[4] = {acc.c[0], acc.c[1], acc.c[2], 0.0};
@@ -379,7 +410,14 @@ MPSG_DI MC<3> fma_fast_d(const MC<3>& acc, const MC<3>& x, double a) {
   qd_add_prenorm(ce, p, t);
   return renorm<3, 5>(t);
 }
-MPSG_DI MC<2> fma_fast_d(const MC<2>& acc, const MC<2>& x, double a) { return add(acc, mul_d(x, a)); }
+MPSG_DI MC<2> fma_acc_d(const MC<2>& acc, const MC<2>& x, double a) { return add(acc, mul_d(x, a)); }
+// canonical form of a fma_acc accumulator before it is stored (once per row)
+MPSG_DI MC<4> canon(const MC<4>& v) {
+  double t[5] = {v.c[0], v.c[1], v.c[2], v.c[3], 0.0};
+  return renorm<4, 5>(t);
+}
+MPSG_DI MC<3> canon(const MC<3>& v) { return v; }
+MPSG_DI MC<2> canon(const MC<2>& v) { return v; }
 
 template <int K>
 MPSG_DI MC<K> zero() {

@@ -62,7 +62,7 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
     if constexpr (!CPLX) {
       if (seg)
         sell_real_seg_kernel<K, MX><<<blocks, 128, 0, st>>>(S, xre, yre, ctx->seg_bounds, ctx->seg_T);
-      else if (order == ORDER_FAST && (K > 2 || MPSG_DD_FUSED) && MPSG_FUSED)
+      else if (order == ORDER_FAST && MPSG_FUSED)
         CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_FAST, MX>, blocks, 128, 0, st, xre, xb, S, xre,
                                  yre));
       else if (sorder == ORDER_SCALAR)
@@ -77,7 +77,7 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
       if (seg)
         sell_complex_kernel<K, ORDER_SCALAR, MX, CONJ, true>
             <<<blocks, 128, 0, st>>>(S, xre, xim, yre, yim, ctx->seg_bounds, ctx->seg_T);
-      else if (order == ORDER_FAST && (K > 2 || MPSG_DD_FUSED) && MPSG_FUSED)
+      else if (order == ORDER_FAST && MPSG_FUSED)
         CUDA_TRY(ctx, launch_win(ctx, sell_complex_kernel<K, ORDER_FAST, MX, CONJ>, blocks, 128, 0, st, xre, xb,
                                  S, xre, xim, yre, yim, nullptr, 1));
       else if (sorder == ORDER_SCALAR)

@@ -60,7 +60,7 @@ struct AVal<K, false> {  // Pure: K component planes, mul(a, v)
   MPSG_DI void load_ldg(const double* __restrict__ vp, int64_t st, int64_t e) { a = load_planes<K>(vp, st, e); }
   MPSG_DI MC<K> times(const MC<K>& v) const { return mul(a, v); }
   // FAST order: acc + a*v with one renormalisation (mc_arith.cuh fma_fast)
-  MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_fast(acc, a, v); }
+  MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_acc(acc, a, v); }
 };
 template <int K>
 struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
@@ -69,7 +69,7 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
   MPSG_DI void load(const double* __restrict__ vp, int64_t, int64_t e) { a = ld_f64_stream(vp + e); }
   MPSG_DI void load_ldg(const double* __restrict__ vp, int64_t, int64_t e) { a = __ldg(vp + e); }
   MPSG_DI MC<K> times(const MC<K>& v) const { return mul_d(v, a); }
-  MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_fast_d(acc, v, a); }
+  MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_acc_d(acc, v, a); }
 };
 
 // ---------------------------------------------------------------------------
@@ -190,6 +190,7 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
         else
           acc = add(acc, a.times(load_aos<K>(x, c[j])));
       }
+    if constexpr (FUSED) acc = canon(acc);
     return acc;
   } else {
     for (; k + G <= len; k += G) {
@@ -534,10 +535,10 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = load_aos<K>(xre, c[u]);
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[0] = fma_fast_d(acc[0], v[u], a[u]);
+      for (int u = 0; u < U; ++u) acc[0] = fma_acc_d(acc[0], v[u], a[u]);
     }
     for (; k < e; k += 32)
-      acc[0] = fma_fast_d(acc[0], load_aos<K>(xre, ld_s32_stream(L.col + k)), ld_f64_stream(L.val + k));
+      acc[0] = fma_acc_d(acc[0], load_aos<K>(xre, ld_s32_stream(L.col + k)), ld_f64_stream(L.val + k));
   } else if constexpr (!CPLX) {
     int c = k < e ? ld_s32_stream(L.col + k) : 0;
     for (; k < e; k += 32) {
