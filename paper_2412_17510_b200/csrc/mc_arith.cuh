@@ -380,7 +380,36 @@ MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   qd_add_prenorm(ce, pv, t);
   return renorm<3, 5>(t);
 }
-MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x) { return fma_fast(acc, a, x); }
+#ifndef MPSG_TD_SWEEP
+#define MPSG_TD_SWEEP 1
+#endif
+MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
+#if MPSG_TD_SWEEP
+  const double ae[4] = {a.c[0], a.c[1], a.c[2], 0.0};
+  const double xe[4] = {x.c[0], x.c[1], x.c[2], 0.0};
+  double p[5];
+  qd_mul_prenorm(ae, xe, p);
+  const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
+  const double ce[4] = {acc.c[0], acc.c[1], acc.c[2], 0.0};
+  double t[5];
+  qd_add_prenorm(ce, pv, t);
+  double s = t[4];
+#pragma unroll
+  for (int i = 3; i >= 0; --i) {
+    double hi, lo;
+    qts(t[i], s, hi, lo);
+    s = hi;
+    t[i + 1] = lo;
+  }
+  MC<3> r;
+  r.c[0] = s;
+  r.c[1] = t[1];
+  r.c[2] = dadd(dadd(t[2], t[3]), t[4]);
+  return r;
+#else
+  return fma_fast(acc, a, x);
+#endif
+}
 // DD: the product's (p1, p2) without its quick_two_sum, straight into the add
 MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) {
   double p1, p2;
@@ -416,7 +445,14 @@ MPSG_DI MC<4> canon(const MC<4>& v) {
   double t[5] = {v.c[0], v.c[1], v.c[2], v.c[3], 0.0};
   return renorm<4, 5>(t);
 }
-MPSG_DI MC<3> canon(const MC<3>& v) { return v; }
+MPSG_DI MC<3> canon(const MC<3>& v) {
+#if MPSG_TD_SWEEP
+  double t[4] = {v.c[0], v.c[1], v.c[2], 0.0};
+  return renorm<3, 4>(t);
+#else
+  return v;
+#endif
+}
 MPSG_DI MC<2> canon(const MC<2>& v) { return v; }
 
 template <int K>
