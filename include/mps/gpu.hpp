@@ -127,8 +127,9 @@ class Context {
 };
 
 // Accumulation order.  Lane4 / Scalar are the reference's lanes-on /
-// lanes-off orders (bit-exact); Fast reorders long rows for throughput and
-// is checked against |y - y_ref| <= 4 * rowlen * u * sum|a||x|.
+// lanes-off orders (bit-exact); Fast reorders long rows and fuses each
+// product-accumulate (one renormalisation per nonzero) for throughput, and is
+// checked against |y - y_ref| <= 4 * rowlen * u * sum|a||x|.
 enum class Order : int { Scalar = MPSG_ORDER_SCALAR, Lane4 = MPSG_ORDER_LANE4, Fast = MPSG_ORDER_FAST };
 inline Order order_of(const KernelMode& m) { return m.lanes_enabled ? Order::Lane4 : Order::Scalar; }
 

@@ -34,8 +34,9 @@
  *    (row_sum_scalar, kernels.hpp:90-99) bit for bit; MPSG_ORDER_LANE4
  *    reproduces the reference default `lanes_enabled = true`
  *    (row_sum_lanes_pure, kernels.hpp:103-121) bit for bit; MPSG_ORDER_FAST
- *    reorders long-row accumulation for throughput and is checked against the
- *    componentwise bound |y - y_ref| <= 4 * rowlen * u * sum|a||x|.
+ *    reorders long-row accumulation and fuses each product-accumulate (one
+ *    renormalisation per nonzero, TD/QD/DD) for throughput, and is checked
+ *    against the componentwise bound |y - y_ref| <= 4 * rowlen * u * sum|a||x|.
  *    KernelMode::threads has no device meaning and is ignored.
  *  - Errors are returned as status codes; nothing crosses the ABI as an
  *    exception.  mpsg_last_error(ctx) gives the message (for MPSG_E_DIM it is
@@ -76,7 +77,7 @@ enum mpsg_status {
 enum mpsg_order {
   MPSG_ORDER_SCALAR = 0, /* lanes off: bit-exact with the reference */
   MPSG_ORDER_LANE4 = 1,  /* lanes on (reference default): bit-exact */
-  MPSG_ORDER_FAST = 2    /* throughput order for long rows (bounded error) */
+  MPSG_ORDER_FAST = 2    /* throughput: long rows reordered, fused product-accumulates (bounded error) */
 };
 
 /* SolverStatus, krylov.hpp:46 */
