@@ -1,0 +1,92 @@
+"""The FAST order's fused product-accumulate (mc_arith.cuh fma_acc / fma_fast:
+one renormalisation per nonzero, the accumulator kept by the renorm's backward
+sweep) against the north-star componentwise bound
+|y - y_ref| <= 4 rowlen u sum|a||x| (u = 2^-104 / 2^-156 / 2^-208), row by row,
+on inputs chosen to stress it: power-law long rows (the long-row kernel's
+chunked chains), a 2^+-60 exponent spread, exact pairwise cancellation, Mixed
+mode, complex.  The worst ratio must stay far inside the bound (the measured
+worst is ~1/30 for TD, ~1/100 for QD; tools/fused_adversarial.py)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2412_17510_b200 as M
+import synth
+from tests.util import bound_ok, mixed_of
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 0.25  # worst |error| / bound allowed here (the contract is 1.0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = M.Context(0)
+    yield c
+    c.close()
+
+
+def _check(A, x, y, K, mixed=False):
+    ok, worst = bound_ok(A, x, y, O.spmv(A, x, 0, mixed=mixed), K)
+    assert ok and worst <= MARGIN, worst
+    return worst
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_fast_power_law_long_rows(ctx, K):
+    c = M.Context(0)
+    c.set_layout(long_threshold=64, sigma=1024, fast_chunk=256)  # many long rows, several chunks each
+    A = synth.config_matrix(4, K, 20000, 6000.0, 1.8)
+    x = synth.config_vector(4, A.nrows, K)
+    _check(A, x, M.spmv(M.DeviceCsr(A, K, ctx=c), x, M.ORDER_FAST), K)
+    c.close()
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_fast_wide_exponent_range(ctx, K):
+    rng = np.random.default_rng(K)
+    A = synth.config_matrix(2, K, 20000, 40.0)
+    A.planes *= np.exp2(rng.integers(-60, 61, A.planes.shape[1])).astype(float)[None, :]
+    x = synth.config_vector(2, A.nrows, K) * np.exp2(rng.integers(-60, 61, A.nrows)).astype(float)[:, None]
+    _check(A, x, M.spmv(M.DeviceCsr(A, K, ctx=ctx), x, M.ORDER_FAST), K)
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_fast_exact_cancellation(ctx, K):
+    A = synth.config_matrix(2, K, 20000, 40.0)
+    A.planes[:, 1::2] = -A.planes[:, 0::2][:, : A.planes[:, 1::2].shape[1]]
+    x = synth.config_vector(2, A.nrows, K)
+    _check(A, x, M.spmv(M.DeviceCsr(A, K, ctx=ctx), x, M.ORDER_FAST), K)
+
+
+@pytest.mark.parametrize("K", [3, 4])
+def test_fast_mixed_mode(ctx, K):
+    A = mixed_of(synth.config_matrix(2, K, 20000, 40.0))
+    x = synth.config_vector(2, A.nrows, K)
+    _check(A, x, M.spmv(M.DeviceCsr(A, K, ctx=ctx, mixed=True), x, M.ORDER_FAST), K, mixed=True)
+
+
+@pytest.mark.parametrize("K", [3, 4])
+def test_fast_complex(ctx, K):
+    A = synth.config_matrix(3, K, 4000, 24.0)
+    xr, xi = synth.config_vector(3, A.nrows, K)
+    yr, yi = M.spmv_complex(M.DeviceCsr(A, K, True, ctx=ctx), xr, xi, M.ORDER_FAST)
+    rr, ri = O.spmv_complex(A, xr, xi, 0)
+    s = O.abs_rowsum(A, A.planes[0], xr) + O.abs_rowsum(A, A.planes[K], xi)
+    s = s + O.abs_rowsum(A, A.planes[0], xi) + O.abs_rowsum(A, A.planes[K], xr)
+    for y, ref in ((yr, rr), (yi, ri)):
+        ok, worst = bound_ok(A, xr, y, ref, K, extra=s)
+        assert ok and worst <= MARGIN, worst
+
+
+def test_fast_output_is_canonical(ctx):
+    """Stored FAST results are renormalised (the per-row canon()): each lower
+    component is at most half an ulp of the one above."""
+    K = 4
+    A = synth.config_matrix(2, K, 20000, 40.0)
+    x = synth.config_vector(2, A.nrows, K)
+    y = M.spmv(M.DeviceCsr(A, K, ctx=ctx), x, M.ORDER_FAST)
+    for j in range(K - 1):
+        hi, lo = y[:, j], y[:, j + 1]
+        nz = hi != 0
+        assert np.all(np.abs(lo[nz]) <= np.spacing(np.abs(hi[nz])) / 2 * (1 + 1e-12))
