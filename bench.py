@@ -273,6 +273,14 @@ class Flush:
         self.acc.add_(self.r.sum())
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            return next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), "unknown")
+    except OSError:
+        return "unknown"
+
+
 def best_reference(steps, warmup, cfg, K):
     """The fastest way the reference computes this SpMV on this host: lanes on
     (its default) and off, its own flags and the x86-64-v3 build (all
@@ -307,7 +315,7 @@ def best_reference(steps, warmup, cfg, K):
     finally:
         O.use_ref_build(False)
     r["sample"] = f"{r['sample']} [fastest reference variant: {label}]"
-    return r, {"unit": "Gnnz/s", "rows": rows, "chosen": label}
+    return r, {"unit": "Gnnz/s", "rows": rows, "chosen": label, "cpu": cpu_model(), "nproc": os.cpu_count()}
 
 
 def setup_stream(torch, M, dev):
