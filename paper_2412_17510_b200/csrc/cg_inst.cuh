@@ -43,6 +43,8 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   const int G = (int)std::max<int64_t>(
       1, std::min<int64_t>({(int64_t)DOT_MAX_BLOCKS, gpol == 0 ? (n + 2047) / 2048 : gwave,
                             (n + DOT_THREADS - 1) / DOT_THREADS}));
+  const char* eoo = std::getenv("MPSG_CG_OWN_OCC");
+  const bool own_occ = !(eoo && eoo[0] == '0');
   cudaGetLastError();
   double *b = nullptr, *x = nullptr, *r = nullptr, *pfull = nullptr, *q = nullptr, *part = nullptr,
          *hist = nullptr, *loc = nullptr, *gath = nullptr, *pend = nullptr;
@@ -85,7 +87,7 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   CG_TRY(cudaMalloc(&r, vb ? vb : 8));
   CG_TRY(cudaMalloc(&pfull, (size_t)std::max<int64_t>(nx, 1) * K * sizeof(double)));
   CG_TRY(cudaMalloc(&q, vb ? vb : 8));
-  CG_TRY(cudaMalloc(&part, (size_t)G * K * sizeof(double)));
+  CG_TRY(cudaMalloc(&part, (size_t)DOT_MAX_BLOCKS * K * sizeof(double)));
   CG_TRY(cudaMalloc(&hist, (size_t)(max_iters + 1) * sizeof(double)));
   CG_TRY(cudaMalloc(&pend, (size_t)(max_iters + 1) * K * sizeof(double)));
   CG_TRY(cudaMalloc(&dst, sizeof(CgState<K>)));
@@ -100,11 +102,28 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
   auto reduce = [&](auto mode_tag, int post, const double* u, const double* v, double* xx, double* rr,
                     int gate) -> int {
     constexpr int MODE = decltype(mode_tag)::value;
-    if (fused)
-      cg_reduce_kernel<K, MODE, true><<<G, DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part, gate,
-                                                                  D ? loc : nullptr);
-    else
-      cg_reduce_kernel<K, MODE><<<G, DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part, gate, D ? loc : nullptr);
+    // this kernel's own resident wave (MPSG_CG_OWN_OCC=0: the shared grid G);
+    // the occupancy is cached per instantiation, the grid follows n
+    auto own_grid = [&](int occ_k) -> int {
+      if (!own_occ) return G;
+      const int64_t w = (int64_t)sms * std::max(occ_k, 1);
+      return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)DOT_MAX_BLOCKS, w,
+                                                          (n + DOT_THREADS - 1) / DOT_THREADS}));
+    };
+    auto occ_of = [](auto kern) {
+      int o = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, DOT_THREADS, 0);
+      return o;
+    };
+    if (fused) {
+      static const int of = occ_of(cg_reduce_kernel<K, MODE, true>);
+      cg_reduce_kernel<K, MODE, true><<<own_grid(of), DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part,
+                                                                             gate, D ? loc : nullptr);
+    } else {
+      static const int ou = occ_of(cg_reduce_kernel<K, MODE>);
+      cg_reduce_kernel<K, MODE><<<own_grid(ou), DOT_THREADS, 0, st>>>(dst, post, n, u, v, xx, rr, part, gate,
+                                                                      D ? loc : nullptr);
+    }
     if (D) {
       int e = allgather_mc(D->comm, loc, gath, K, st);
       if (e) return e;
