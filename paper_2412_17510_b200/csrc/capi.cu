@@ -19,6 +19,8 @@
 
 #include "internal.h"
 
+#include <omp.h>
+
 using namespace mpsg;
 
 namespace {
@@ -199,6 +201,73 @@ int spmv_host_overlapped(mpsg_ctx* ctx, const mpsg_csr* A, int order, const doub
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   return MPSG_OK;
 }
+// ---- pageable host vectors ---------------------------------------------
+// A std::vector / numpy array is pageable: the driver's own staging copies run
+// at ~16 GB/s.  Instead: 8 MB chunks through two pinned slots, the host-side
+// copy into / out of a slot done by OpenMP threads while the other slot's DMA
+// runs (MPSG_STAGE_HOST=0 falls back to the driver).
+constexpr size_t HCHUNK = 8u << 20;
+bool host_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+int ensure_hslots(mpsg_ctx* ctx) {
+  if (ctx->hslot_cap >= HCHUNK) return MPSG_OK;
+  for (int i = 0; i < 2; ++i) {
+    CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->hslot[i]), HCHUNK, cudaHostAllocDefault));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->hslot_ev[i], cudaEventDisableTiming));
+  }
+  ctx->hslot_cap = HCHUNK;
+  return MPSG_OK;
+}
+void par_copy(void* dst, const void* src, size_t n) {
+  const int T = (int)std::min<size_t>(8, std::max<size_t>(1, n >> 20));  // >= 1 MB per thread
+#pragma omp parallel for num_threads(T) schedule(static)
+  for (int t = 0; t < T; ++t) {
+    const size_t a = n * (size_t)t / (size_t)T, b = n * (size_t)(t + 1) / (size_t)T;
+    std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+  }
+}
+int h2d_staged(mpsg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  size_t i = 0;
+  for (size_t off = 0; off < bytes; off += HCHUNK, ++i) {
+    const int sl = (int)(i & 1);
+    const size_t len = std::min(HCHUNK, bytes - off);
+    if (i >= 2) CUDA_TRY(ctx, cudaEventSynchronize(ctx->hslot_ev[sl]));
+    par_copy(ctx->hslot[sl], static_cast<const char*>(src) + off, len);
+    CUDA_TRY(ctx, cudaMemcpyAsync(static_cast<char*>(dst) + off, ctx->hslot[sl], len, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->hslot_ev[sl], st));
+  }
+  return MPSG_OK;
+}
+int d2h_staged(mpsg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  int psl = -1;
+  size_t poff = 0, plen = 0, i = 0;
+  for (size_t off = 0; off < bytes; off += HCHUNK, ++i) {
+    const int sl = (int)(i & 1);
+    const size_t len = std::min(HCHUNK, bytes - off);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hslot[sl], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                  st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->hslot_ev[sl], st));
+    if (psl >= 0) {  // the previous chunk drains while this one crosses PCIe
+      CUDA_TRY(ctx, cudaEventSynchronize(ctx->hslot_ev[psl]));
+      par_copy(static_cast<char*>(dst) + poff, ctx->hslot[psl], plen);
+    }
+    psl = sl;
+    poff = off;
+    plen = len;
+  }
+  if (psl >= 0) {
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->hslot_ev[psl]));
+    par_copy(static_cast<char*>(dst) + poff, ctx->hslot[psl], plen);
+  }
+  return MPSG_OK;
+}
+
 bool can_overlap(const mpsg_ctx* ctx, const mpsg_csr* A) {
   return ctx->overlap && ctx->copy && A->part_slice.size() >= 3 && A->part_slice.size() <= 17;
 }
@@ -247,6 +316,7 @@ int mpsg_ctx_create(int device, mpsg_ctx** out) {
   if (const char* s = std::getenv("MPSG_FAST_CHUNK")) ctx->fast_chunk = std::atoll(s);
   if (const char* s = std::getenv("MPSG_COLBLOCK_BYTES")) ctx->colblock_bytes = std::atoll(s);
   if (const char* s = std::getenv("MPSG_OVERLAP")) ctx->overlap = s[0] != '0';
+  if (const char* s = std::getenv("MPSG_STAGE_HOST")) ctx->stage_host = s[0] != '0';
   if (const char* s = std::getenv("MPSG_COLBLOCK_MIN")) ctx->colblock_min = std::atoll(s);
   *out = ctx;
   return MPSG_OK;
@@ -257,6 +327,10 @@ void mpsg_ctx_destroy(mpsg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (auto& p : ctx->dbuf)
     if (p) cudaFree(p);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->hslot[i]) cudaFreeHost(ctx->hslot[i]);
+    if (ctx->hslot_ev[i]) cudaEventDestroy(ctx->hslot_ev[i]);
+  }
   if (ctx->seg_bounds) cudaFree(ctx->seg_bounds);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -611,6 +685,27 @@ int mpsg_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen, const d
   if ((rc = ensure_scratch(ctx, 0, xb))) return rc;
   if ((rc = ensure_scratch(ctx, 1, yb))) return rc;
   cudaStream_t st = ctx->stream;
+  const bool px = xb && host_pageable(x), py = yb && host_pageable(y);
+  if (ctx->stage_host && (px || py) && ensure_hslots(ctx) == MPSG_OK) {
+    // pageable vectors: chunked pinned staging both ways
+    if (px)
+      rc = h2d_staged(ctx, ctx->dbuf[0], x, xb, st);
+    else if (xb)
+      rc = cudaMemcpyAsync(ctx->dbuf[0], x, xb, cudaMemcpyHostToDevice, st) == cudaSuccess
+               ? MPSG_OK
+               : fail(ctx, MPSG_E_CUDA, "spmv: x copy failed");
+    if (rc) return rc;
+    if ((rc = launch_spmv(ctx, A, order, ctx->dbuf[0], nullptr, ctx->dbuf[1], nullptr, st))) return rc;
+    if (py)
+      rc = d2h_staged(ctx, y, ctx->dbuf[1], yb, st);
+    else if (yb)
+      rc = cudaMemcpyAsync(y, ctx->dbuf[1], yb, cudaMemcpyDeviceToHost, st) == cudaSuccess
+               ? MPSG_OK
+               : fail(ctx, MPSG_E_CUDA, "spmv: y copy failed");
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    return MPSG_OK;
+  }
   if (xb) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dbuf[0], x, xb, cudaMemcpyHostToDevice, st));
   if (can_overlap(ctx, A))
     return spmv_host_overlapped(ctx, A, order, ctx->dbuf[0], nullptr, ctx->dbuf[1], nullptr, y, nullptr, false);

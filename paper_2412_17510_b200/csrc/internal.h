@@ -32,6 +32,12 @@ struct mpsg_ctx {
   int seg_T = 1;
   std::vector<int64_t> seg_host;
   std::string err;
+  // pinned staging for pageable host vectors (two chunk slots, double-buffered
+  // against the DMA; the host side copies with OpenMP threads)
+  double* hslot[2] = {nullptr, nullptr};
+  size_t hslot_cap = 0;
+  cudaEvent_t hslot_ev[2] = {nullptr, nullptr};
+  bool stage_host = true;         // MPSG_STAGE_HOST=0 disables
   // scratch for host-pointer calls
   double* dbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t dcap[4] = {0, 0, 0, 0};
