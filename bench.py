@@ -54,13 +54,14 @@ OPS_PER_NNZ = {2: 20, 3: 202, 4: 206}
 # Mixed mode (binary64 matrix): one mul_by_double + one add
 OPS_PER_NNZ_MIXED = {2: 17, 3: 130, 4: 152}
 # FAST order executes a fused product-accumulate (mc_arith.cuh fma_acc /
-# fma_fast): the product's pre-normalisation terms go straight into the add
-# (QD: 99 + 1 + 63 + a 12-op renorm sweep + 1 = 176; TD: 99 + 1 + 63 + 12 + 2 =
-# 177; DD: 6 + 11 = 17), one canonicalising renorm per row (QD 22, TD 16), and
+# fma_fast): the running accumulator is updated level by level (QD: 6
+# two_prods 12 + 14 two_sums 84 + level-3 sum 16 + sweep 9 = 121; TD: 6 + 5
+# two_sums 30 + level-2 sum 10 + sweep 6 = 52; DD: 6 + 11 = 17), one
+# canonicalising renorm per row (QD 22, TD 16), and
 # stored vector updates with the add's full renorm (QD 185, TD 183).  The roofline of
 # a FAST line counts the operations it executes; the reference's count and the
 # fraction against it are reported beside (reference_fp64_ops, reference_frac).
-OPS_FAST = {2: 17, 3: 177, 4: 176}
+OPS_FAST = {2: 17, 3: 52, 4: 121}
 OPS_FAST_MIXED = {2: 17, 3: 114, 4: 122}
 OPS_FAST_UPDATE = {2: 20, 3: 183, 4: 185}
 ROW_CANON = {2: 0, 3: 16, 4: 22}

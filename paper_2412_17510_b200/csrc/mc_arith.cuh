@@ -326,11 +326,14 @@ MPSG_DI MC<4> mul_d(const MC<4>& x, double y) {  // multicomp.hpp:273-277
 //    last two merged) straight into qd_add_prenorm, then the add's full
 //    renorm_n -- skips the product's own renormalisation.  Used where the
 //    result is stored (vector updates).
-//  * fma_acc: the same, but the running accumulator keeps only the backward
-//    quick-two-sum sweep of renorm_n (the forward collect that canonicalises
-//    zero components is left to canon() once per row): QD 176 instead of 206
-//    fp64 operations per nonzero; worst 1/100 of the bound on the adversarial
-//    probes (long rows, 2^+-60 exponent spread, exact cancellation).
+//  * fma_acc: the running row / dot accumulator, summed level by level
+//    (MPSG_QD_LEVELS, below) and kept by a backward quick-two-sum sweep only
+//    (the forward collect that canonicalises zero components is left to
+//    canon() once per row): QD 121 and TD 52 fp64 operations per nonzero
+//    instead of 206 / 202; worst 0.15 (QD) / 0.18 (TD) of the bound on the
+//    adversarial probes (long rows, 2^+-60 exponent spread, exact
+//    cancellation).  MPSG_QD_LEVELS=0 builds the previous prenorm-chained
+//    accumulate (QD 176 operations, worst 0.009).
 // ---------------------------------------------------------------------------
 MPSG_DI MC<4> renorm_sweep(double (&t)[5]) {  // renorm_n<4,5>'s backward sweep, tail merged
   double s = t[4];
@@ -363,12 +366,64 @@ MPSG_DI MC<4> fma_fast(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
   const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
   return qd_fused<false>(acc, pv);
 }
+#ifndef MPSG_QD_LEVELS
+#define MPSG_QD_LEVELS 1
+#endif
+#if MPSG_QD_LEVELS
+// Level-wise QD product-accumulate: acc + a*x summed by magnitude level
+// (level k = terms of order 2^-53k): each level's terms chained through
+// two_sums whose errors drop to the next level; level 3 is a plain sum, small
+// terms first and the accumulator's own c3 last; then the backward sweep.
+// 121 fp64 operations instead of 176 (product and add prenorms + sweep).
+// The dropped terms are the ones the reference's qd_mul_prenorm drops
+// (a1x3, a2x2, a3x1 and the errors of the order-3 products).
+MPSG_DI MC<4> fma_acc(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
+  two_prod(a.c[0], x.c[0], p0, q0);
+  two_prod(a.c[0], x.c[1], p1, q1);
+  two_prod(a.c[1], x.c[0], p2, q2);
+  two_prod(a.c[0], x.c[2], p3, q3);
+  two_prod(a.c[1], x.c[1], p4, q4);
+  two_prod(a.c[2], x.c[0], p5, q5);
+  double s0, e0, u, f1, f2, f3, f4, s1, v, g[9], s2;
+  two_sum(acc.c[0], p0, s0, e0);  // level 0
+  two_sum(acc.c[1], p1, u, f1);   // level 1: c1 p1 p2 q0 e0
+  two_sum(u, p2, u, f2);
+  two_sum(u, q0, u, f3);
+  two_sum(u, e0, s1, f4);
+  two_sum(acc.c[2], p3, v, g[0]);  // level 2: c2 p3 p4 p5 q1 q2 f1..f4
+  two_sum(v, p4, v, g[1]);
+  two_sum(v, p5, v, g[2]);
+  two_sum(v, q1, v, g[3]);
+  two_sum(v, q2, v, g[4]);
+  two_sum(v, f1, v, g[5]);
+  two_sum(v, f2, v, g[6]);
+  two_sum(v, f3, v, g[7]);
+  two_sum(v, f4, s2, g[8]);
+  double w = g[0];  // level 3
+#pragma unroll
+  for (int i = 1; i < 9; ++i) w = dadd(w, g[i]);
+  w = dadd(dadd(dadd(w, q3), q4), q5);
+  w = dfma(a.c[0], x.c[3], w);
+  w = dfma(a.c[1], x.c[2], w);
+  w = dfma(a.c[2], x.c[1], w);
+  w = dfma(a.c[3], x.c[0], w);
+  w = dadd(w, acc.c[3]);
+  MC<4> r;
+  double h;
+  qts(s2, w, h, r.c[3]);
+  qts(s1, h, h, r.c[2]);
+  qts(s0, h, r.c[0], r.c[1]);
+  return r;
+}
+#else
 MPSG_DI MC<4> fma_acc(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
   double p[5];
   qd_mul_prenorm(a.c, x.c, p);
   const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
   return qd_fused<true>(acc, pv);
 }
+#endif
 MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   const double ae[4] = {a.c[0], a.c[1], a.c[2], 0.0};
   const double xe[4] = {x.c[0], x.c[1], x.c[2], 0.0};
@@ -383,6 +438,34 @@ MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
 #ifndef MPSG_TD_SWEEP
 #define MPSG_TD_SWEEP 1
 #endif
+#if MPSG_QD_LEVELS
+// Level-wise TD product-accumulate (as the QD one above, one level fewer):
+// levels 0-1 through two_sums, level 2 a plain sum (small terms first, the
+// accumulator's c2 last), then the backward sweep.  52 fp64 operations instead
+// of 177 (the reference's TD runs the QD chains on zero-extended operands).
+MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
+  double p0, q0, p1, q1, p2, q2;
+  two_prod(a.c[0], x.c[0], p0, q0);
+  two_prod(a.c[0], x.c[1], p1, q1);
+  two_prod(a.c[1], x.c[0], p2, q2);
+  double s0, e0, u, f1, f2, f3, f4, s1;
+  two_sum(acc.c[0], p0, s0, e0);  // level 0
+  two_sum(acc.c[1], p1, u, f1);   // level 1: c1 p1 p2 q0 e0
+  two_sum(u, p2, u, f2);
+  two_sum(u, q0, u, f3);
+  two_sum(u, e0, s1, f4);
+  double w = dadd(dadd(dadd(dadd(dadd(f1, f2), f3), f4), q1), q2);  // level 2
+  w = dfma(a.c[0], x.c[2], w);
+  w = dfma(a.c[1], x.c[1], w);
+  w = dfma(a.c[2], x.c[0], w);
+  w = dadd(w, acc.c[2]);
+  MC<3> r;
+  double h;
+  qts(s1, w, h, r.c[2]);
+  qts(s0, h, r.c[0], r.c[1]);
+  return r;
+}
+#else
 MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
 #if MPSG_TD_SWEEP
   const double ae[4] = {a.c[0], a.c[1], a.c[2], 0.0};
@@ -410,6 +493,7 @@ MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   return fma_fast(acc, a, x);
 #endif
 }
+#endif
 // DD: the product's (p1, p2) without its quick_two_sum, straight into the add
 MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) {
   double p1, p2;
