@@ -75,10 +75,28 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 // ---------------------------------------------------------------------------
 // Row-sum building blocks for the SELL kernels (slot stride 32).
 // ---------------------------------------------------------------------------
-#ifdef MPSG_SELL_MINB
-#define MPSG_SELL_LB __launch_bounds__(128, MPSG_SELL_MINB)
+// 8 resident blocks of 128 threads (64 registers): measured +4-7% on the FAST
+// TD/QD short-row kernels (profiles/r01b_variants.txt, item 36); MPSG_SELL_MINB=0
+// removes the cap.
+#ifndef MPSG_SELL_MINB
+#define MPSG_SELL_MINB 8
+#endif
+// TD/QD only: DD (memory-latency-bound) keeps the compiler's own allocation --
+// minBlocks 0 compiles to the same SASS as no bound (40 registers, 32 in Mixed
+// mode); a 64 cap let it grow (cfg5 DD 228 -> 197 Gnnz/s) and a 12-block cap
+// changed its schedule (-6%).
+#if MPSG_SELL_MINB > 0
+#define MPSG_SELL_LB __launch_bounds__(128, (K == 2 ? 0 : MPSG_SELL_MINB))
 #else
 #define MPSG_SELL_LB __launch_bounds__(128)
+#endif
+
+// Products per round of the FAST QD short-row chain.  With the level-wise
+// accumulate (121 ops) the QD kernel is latency-limited: four products in
+// flight under a 64-register cap (MPSG_SELL_MINB 8) beat two (cfg2 QD 91.1 ->
+// 99.8 Gnnz/s); TD (52 ops) keeps two (G = 4 for TD: 126.3 -> 122.1).
+#ifndef MPSG_FUSED_G_QD
+#define MPSG_FUSED_G_QD 4
 #endif
 
 // Product term of slot-row element k.
@@ -142,7 +160,7 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
 template <int K, bool MX, bool FUSED = false>
 MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
                          const double* __restrict__ x, int len) {
-  constexpr int G = K == 2 ? 4 : 2;
+  constexpr int G = K == 2 ? 4 : (FUSED ? (K == 4 ? MPSG_FUSED_G_QD : 2) : 2);
   constexpr bool PF = K != 2;
   MC<K> acc = zero<K>();
   int k = 0;
