@@ -360,14 +360,24 @@ MPSG_DI MC<4> qd_fused(const MC<4>& acc, const double (&pv)[4]) {
   else
     return renorm<4, 5>(t);
 }
+#ifndef MPSG_QD_LEVELS
+#define MPSG_QD_LEVELS 1
+#endif
+MPSG_DI MC<4> canon(const MC<4>& v);
+MPSG_DI MC<3> canon(const MC<3>& v);
+#if MPSG_QD_LEVELS
+MPSG_DI MC<4> fma_acc(const MC<4>& acc, const MC<4>& a, const MC<4>& x);
+MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x);
+// stored updates: the level-wise accumulate, then the full renormalisation
+// (QD 121 + 22, TD 52 + 16 operations instead of 185 / 183)
+MPSG_DI MC<4> fma_fast(const MC<4>& acc, const MC<4>& a, const MC<4>& x) { return canon(fma_acc(acc, a, x)); }
+#else
 MPSG_DI MC<4> fma_fast(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
   double p[5];
   qd_mul_prenorm(a.c, x.c, p);
   const double pv[4] = {p[0], p[1], p[2], dadd(p[3], p[4])};
   return qd_fused<false>(acc, pv);
 }
-#ifndef MPSG_QD_LEVELS
-#define MPSG_QD_LEVELS 1
 #endif
 #if MPSG_QD_LEVELS
 // Level-wise QD product-accumulate: acc + a*x summed by magnitude level
@@ -424,6 +434,9 @@ MPSG_DI MC<4> fma_acc(const MC<4>& acc, const MC<4>& a, const MC<4>& x) {
   return qd_fused<true>(acc, pv);
 }
 #endif
+#if MPSG_QD_LEVELS
+MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) { return canon(fma_acc(acc, a, x)); }
+#else
 MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   const double ae[4] = {a.c[0], a.c[1], a.c[2], 0.0};
   const double xe[4] = {x.c[0], x.c[1], x.c[2], 0.0};
@@ -435,6 +448,7 @@ MPSG_DI MC<3> fma_fast(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
   qd_add_prenorm(ce, pv, t);
   return renorm<3, 5>(t);
 }
+#endif
 #ifndef MPSG_TD_SWEEP
 #define MPSG_TD_SWEEP 1
 #endif
