@@ -62,7 +62,7 @@ OPS_PER_NNZ_MIXED = {2: 17, 3: 130, 4: 152}
 # a FAST line counts the operations it executes; the reference's count and the
 # fraction against it are reported beside (reference_fp64_ops, reference_frac).
 OPS_FAST = {2: 17, 3: 52, 4: 121}
-OPS_FAST_MIXED = {2: 17, 3: 114, 4: 122}
+OPS_FAST_MIXED = {2: 17, 3: 114, 4: 76}
 OPS_FAST_UPDATE = {2: 20, 3: 68, 4: 143}
 ROW_CANON = {2: 0, 3: 16, 4: 22}
 K_NAME = {2: "DD", 3: "TD", 4: "QD"}
