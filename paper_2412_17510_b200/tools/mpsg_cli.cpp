@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <thread>
 #include <numeric>
 #include <sstream>
 #include <stdexcept>
@@ -289,6 +290,16 @@ mpsg_csr* upload(mpsg_ctx* ctx, const Csr& A, int K, bool cplx, bool mixed, bool
   return d;
 }
 
+// Context creation, retried a few times: a device-initialisation failure can be
+// transient while another process on the GPU is tearing its context down.
+static bool open_ctx(int device, mpsg_ctx** ctx) {
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    if (mpsg_ctx_create(device, ctx) == MPSG_OK) return true;
+    std::this_thread::sleep_for(std::chrono::milliseconds(250));
+  }
+  return false;
+}
+
 int run_spmv(const Args& a) {
   const Coo coo = parse_mtx(a.path);
   const Csr A = coo_to_csr(coo);
@@ -298,7 +309,7 @@ int run_spmv(const Args& a) {
   const int order = order_of(a.lanes);
   if (a.reps < 1) die("time_kernel: repetitions must be at least 1");
   mpsg_ctx* ctx = nullptr;
-  if (mpsg_ctx_create(a.device, &ctx) != MPSG_OK) die("no usable sm_100a GPU", 1);
+  if (!open_ctx(a.device, &ctx)) die("no usable sm_100a GPU", 1);
   mpsg_csr* d = upload(ctx, A, K, cplx, mixed, a.transposed);
   const int64_t n = A.ncols;
   std::vector<double> vr((size_t)n * K), vi(cplx ? (size_t)n * K : 0), yr((size_t)n * K), yi(vi.size());
@@ -352,7 +363,7 @@ int run_solve(const Args& a) {
   if (A.nrows != A.ncols) die("solve: the matrix must be square", 1);
   const int K = precision_k(a.precision);
   mpsg_ctx* ctx = nullptr;
-  if (mpsg_ctx_create(a.device, &ctx) != MPSG_OK) die("no usable sm_100a GPU", 1);
+  if (!open_ctx(a.device, &ctx)) die("no usable sm_100a GPU", 1);
   mpsg_csr* d = upload(ctx, A, K, false, mixed, method == MPSG_BICG);
   const int64_t n = A.ncols;
   const int threads = a.threads > 0 ? a.threads : 1;
