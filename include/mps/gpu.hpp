@@ -45,10 +45,15 @@
 //    SolverReport, never thrown (krylov.hpp:46, 203-213).
 //  * host-vector calls are synchronous, like the reference.
 //
-// The reference-signature drop-ins upload a matrix once and cache it by
-// address (+ a structural fingerprint).  A caller that rewrites a matrix's
-// values in place between calls must call mps::gpu::invalidate(A) (or hold
-// an explicit DeviceCsr).
+// The reference-signature drop-ins upload a matrix once and cache it, keyed
+// by its address, buffer pointers, shape and a content fingerprint (a hash of
+// up to 2 x 1024 evenly spaced entries of indptr, indices and every value
+// plane, plus the first and last of each).  A matrix destroyed and rebuilt at
+// the same address with the same buffers is therefore caught unless the two
+// agree on every sampled entry; at most kCacheEntries matrices per element
+// type stay resident (least recently used evicted).  A caller that rewrites
+// values in place between calls -- which the sample can miss -- must call
+// mps::gpu::invalidate(A), or hold an explicit DeviceCsr (no cache at all).
 #pragma once
 
 #include <cstdint>
@@ -100,6 +105,9 @@ void planes_of(const CsrMatrix<MultiComponent<K>>& A, const double** out) {
   for (int j = 0; j < K; ++j) out[j] = A.values.component(j);  // sparse.hpp:63
 }
 inline void planes_of(const CsrMatrix<double>& A, const double** out) { out[0] = A.values.data(); }
+template <int K>
+constexpr int nplanes(const CsrMatrix<MultiComponent<K>>*) { return K; }
+constexpr int nplanes(const CsrMatrix<double>*) { return 1; }
 }  // namespace detail
 
 // ---------------------------------------------------------------- context
@@ -107,7 +115,7 @@ class Context {
  public:
   explicit Context(int device = 0) {
     int rc = mpsg_ctx_create(device, &ctx_);
-    if (rc != MPSG_OK) throw std::runtime_error("mpsg_ctx_create failed: no usable sm_100a GPU");
+    if (rc != MPSG_OK) throw std::runtime_error(std::string("no usable sm_100a GPU: ") + mpsg_create_error());
   }
   ~Context() { mpsg_ctx_destroy(ctx_); }
   Context(const Context&) = delete;
@@ -250,43 +258,87 @@ ComplexVector<F> sptmv_complex(const DeviceCsr<E, F>& A, const ComplexVector<F>&
 
 // --------------------------------------------------- upload cache (drop-in)
 namespace detail {
+constexpr std::size_t kCacheEntries = 8;
 struct CacheKey {
   const void* addr;
   const void* indptr;
   const void* plane0;
-  std::int64_t nnz;
+  std::int64_t nnz, nrows, ncols;
+  std::uint64_t fp;  // content fingerprint (fingerprint() below)
   bool operator<(const CacheKey& o) const {
-    return std::tie(addr, indptr, plane0, nnz) < std::tie(o.addr, o.indptr, o.plane0, o.nnz);
+    return std::tie(addr, indptr, plane0, nnz, nrows, ncols, fp) <
+           std::tie(o.addr, o.indptr, o.plane0, o.nnz, o.nrows, o.ncols, o.fp);
   }
 };
+// FNV-1a over up to 1024 evenly spaced elements of an array plus its last one
+// (O(1) in the matrix size: a cache hit must stay cheap next to the SpMV).
+template <class T>
+void fnv_sample(std::uint64_t& h, const T* p, std::int64_t n) {
+  if (n <= 0 || !p) return;
+  const std::int64_t step = n > 1024 ? n / 1024 : 1;
+  auto mix = [&](const T& v) {
+    unsigned char b[sizeof(T)];
+    std::memcpy(b, &v, sizeof(T));
+    for (unsigned char c : b) h = (h ^ c) * 1099511628211ull;
+  };
+  for (std::int64_t i = 0; i < n; i += step) mix(p[i]);
+  mix(p[n - 1]);
+}
+template <class E>
+std::uint64_t fingerprint(const CsrMatrix<E>& A) {
+  std::uint64_t h = 1469598103934665603ull;
+  fnv_sample(h, A.indptr.data(), static_cast<std::int64_t>(A.indptr.size()));
+  fnv_sample(h, A.indices.data(), static_cast<std::int64_t>(A.indices.size()));
+  const double* p[16];
+  planes_of(A, p);
+  for (int j = 0; j < nplanes(&A); ++j) fnv_sample(h, p[j], A.nnz());
+  return h;
+}
 template <class E, class F>
-std::map<CacheKey, std::shared_ptr<DeviceCsr<E, F>>>& cache() {
-  static std::map<CacheKey, std::shared_ptr<DeviceCsr<E, F>>> c;
+struct CacheEntry {
+  std::shared_ptr<DeviceCsr<E, F>> dev;
+  std::uint64_t last_use;
+};
+template <class E, class F>
+std::map<CacheKey, CacheEntry<E, F>>& cache() {
+  static std::map<CacheKey, CacheEntry<E, F>> c;
   return c;
+}
+inline std::uint64_t& use_clock() {
+  static std::uint64_t t = 0;
+  return t;
 }
 template <class E>
 CacheKey key_of(const CsrMatrix<E>& A) {
   const double* p[16];
   planes_of(A, p);
-  return {&A, A.indptr.data(), p[0], A.nnz()};
+  return {&A, A.indptr.data(), p[0], A.nnz(), A.nrows, A.ncols, fingerprint(A)};
 }
 template <class E>
 CacheKey key_of(const ComplexSparseMatrix<E>& A) {
   const double* p[16];
   planes_of(A.re, p);
-  return {&A, A.re.indptr.data(), p[0], A.re.nnz()};
+  const std::uint64_t fp = fingerprint(A.re) * 31u + fingerprint(A.im);
+  return {&A, A.re.indptr.data(), p[0], A.re.nnz(), A.re.nrows, A.re.ncols, fp};
 }
 template <class E, class F, class M>
 const DeviceCsr<E, F>& cached(const M& A, bool need_transpose) {
   auto& c = cache<E, F>();
   const CacheKey k = key_of(A);
   auto it = c.find(k);
-  if (it == c.end() || (need_transpose && !it->second->has_transpose())) {
+  if (it == c.end() || (need_transpose && !it->second.dev->has_transpose())) {
     // drop stale entries for the same address (rebuilt matrix / no transpose yet)
     for (auto jt = c.begin(); jt != c.end();) jt = (jt->first.addr == k.addr) ? c.erase(jt) : std::next(jt);
-    it = c.emplace(k, std::make_shared<DeviceCsr<E, F>>(A, need_transpose)).first;
+    while (c.size() >= kCacheEntries) {  // evict the least recently used
+      auto lru = c.begin();
+      for (auto jt = c.begin(); jt != c.end(); ++jt)
+        if (jt->second.last_use < lru->second.last_use) lru = jt;
+      c.erase(lru);
+    }
+    it = c.emplace(k, CacheEntry<E, F>{std::make_shared<DeviceCsr<E, F>>(A, need_transpose), 0}).first;
   }
-  return *it->second;
+  it->second.last_use = ++use_clock();
+  return *it->second.dev;
 }
 template <class M>
 void invalidate_addr(const M& A) {

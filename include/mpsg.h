@@ -168,6 +168,10 @@ typedef struct mpsg_cg_report {
 
 /* ---- context --------------------------------------------------------- */
 MPSG_API int mpsg_ctx_create(int device, mpsg_ctx** out);
+/* Why the last mpsg_ctx_create on this host thread failed ("" if it did not):
+ * the CUDA error name and text.  A device held by another process
+ * (cudaErrorDevicesUnavailable) is retried inside mpsg_ctx_create for ~2 s. */
+MPSG_API const char* mpsg_create_error(void);
 MPSG_API void mpsg_ctx_destroy(mpsg_ctx* ctx);
 MPSG_API const char* mpsg_last_error(const mpsg_ctx* ctx);
 /* Use a caller-owned cudaStream_t (as void*) for subsequent work; NULL

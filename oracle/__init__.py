@@ -68,6 +68,8 @@ def orc():
         L.orc_checksum_complex.restype = _u64
         L.orc_exact_diff.argtypes = [_i32, _P, _P]
         L.orc_exact_diff.restype = _f64
+        L.orc_exact_diff_vec.argtypes = [_i32, _i64, _P, _P, _P]
+        L.orc_exact_diff_vec.restype = None
         L.orc_abs_rowsum.argtypes = [_i32, _i64, _P, _P, _P, _P, _P]
         L.orc_cg.argtypes = [_i32, _i32, _i64, _P, _P, _P, _P, _f64, _f64, _i64, _P, _P, _P, _P,
                              _P, _P]
@@ -168,10 +170,8 @@ def exact_absdiff(a, b) -> np.ndarray:
     """|a_i - b_i| (exact difference, rounded once) for AoS [n,K] arrays."""
     a, b = _c(a), _c(b)
     K = a.shape[1]
-    L = orc()
     out = np.empty(a.shape[0])
-    for i in range(a.shape[0]):
-        out[i] = L.orc_exact_diff(K, _p(a[i]), _p(b[i]))
+    orc().orc_exact_diff_vec(K, a.shape[0], _p(a), _p(b), _p(out))
     return out
 
 
@@ -413,15 +413,6 @@ class RefCVec:
     def __del__(self):
         if getattr(self, "h", None):
             ref().ref_cvec_destroy(self.h)
-
-
-def ref_spmv_complex(A, xre, xim, order=LANE4, threads=1):
-    K = xre.shape[1]
-    Ah, xh, yh = RefComplex(A, K), RefCVec(xre, xim), RefCVec(K=K)
-    rc = ref().ref_spmv_complex(Ah.h, xh.h, order, threads, yh.h)
-    if rc != 0:
-        raise ValueError(ref().ref_last_error().decode())
-    return yh.read(A.nrows)
 
 
 def ref_mc_op(op: str, K: int, a, b=None):

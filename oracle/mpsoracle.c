@@ -526,6 +526,11 @@ ORC_API double orc_exact_diff(int K, const double *a, const double *b) {
   return fabs(s);
 }
 
+/* orc_exact_diff over n AoS rows (the full-size bound checks). */
+ORC_API void orc_exact_diff_vec(int K, int64_t n, const double *a, const double *b, double *out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = orc_exact_diff(K, a + i * K, b + i * K);
+}
+
 /* Per-row sum_j |a_ij| |x_j| on leading components, and row lengths.
  * For complex, the caller passes the re/im planes and sums all four. */
 ORC_API void orc_abs_rowsum(int K, int64_t nrows, const int64_t *indptr, const int64_t *indices,

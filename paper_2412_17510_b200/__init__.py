@@ -83,7 +83,7 @@ class _CgReport(ctypes.Structure):
 _lib = None
 
 # every symbol include/mpsg.h declares
-EXPORTS = ("mpsg_ctx_create", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_set_stream",
+EXPORTS = ("mpsg_ctx_create", "mpsg_create_error", "mpsg_ctx_destroy", "mpsg_last_error", "mpsg_ctx_set_stream",
            "mpsg_ctx_set_layout", "mpsg_ctx_synchronize", "mpsg_csr_upload", "mpsg_csr_destroy",
            "mpsg_csr_get_stats", "mpsg_spmv", "mpsg_spmv_dev", "mpsg_spmv_complex",
            "mpsg_spmv_complex_dev", "mpsg_cg", "mpsg_partition_rows", "mpsg_checksum",
@@ -108,6 +108,8 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     L.mpsg_ctx_create.argtypes = [_i32, ctypes.POINTER(_P)]
     L.mpsg_ctx_destroy.argtypes = [_P]
+    L.mpsg_create_error.argtypes = []
+    L.mpsg_create_error.restype = ctypes.c_char_p
     L.mpsg_last_error.argtypes = [_P]
     L.mpsg_last_error.restype = ctypes.c_char_p
     L.mpsg_ctx_set_stream.argtypes = [_P, _P]
@@ -166,10 +168,15 @@ def _p(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(_P)
 
 
-def _aos(v, name="vector") -> np.ndarray:
+def _aos(v, name="vector", K: int | None = None) -> np.ndarray:
+    """(n, K) float64 C-contiguous view of v.  With K given, the component
+    count must match the matrix: the C ABI copies n*K doubles each way, so a
+    narrower vector would be read (and its result written) past its end."""
     a = np.ascontiguousarray(v, dtype=np.float64)
     if a.ndim != 2 or a.shape[1] not in (2, 3, 4):
         raise ValueError(f"{name}: expected an (n, K) float64 array with K in 2..4, got {a.shape}")
+    if K is not None and a.shape[1] != K:
+        raise ValueError(f"{name}: vector has K={a.shape[1]} components, matrix has K={K}")
     return a
 
 
@@ -182,7 +189,7 @@ class Context:
         h = _P()
         rc = lib().mpsg_ctx_create(device, ctypes.byref(h))
         if rc != E_OK:
-            raise MpsgError(rc, f"mpsg_ctx_create(device={device}) failed (no usable GPU?)")
+            raise MpsgError(rc, f"no usable sm_100a GPU: {lib().mpsg_create_error().decode()}")
         self.h = h
 
     def check(self, rc: int):
@@ -300,9 +307,7 @@ def _order(mode) -> int:
 
 def spmv(A: DeviceCsr, v, mode: KernelMode | int | None = None) -> np.ndarray:
     """y = A v (kernels.hpp:348-366); host arrays in, host array out."""
-    x = _aos(v, "spmv")
-    if x.shape[1] != A.K:
-        raise ValueError(f"spmv: vector has K={x.shape[1]} components, matrix has K={A.K}")
+    x = _aos(v, "spmv", A.K)
     y = np.empty((A.nrows, A.K))
     A.ctx.check(lib().mpsg_spmv(A.ctx.h, A.h, _order(mode), x.shape[0], _p(x), _p(y)))
     return y
@@ -310,7 +315,7 @@ def spmv(A: DeviceCsr, v, mode: KernelMode | int | None = None) -> np.ndarray:
 
 def spmv_complex(A: DeviceCsr, v_re, v_im, mode: KernelMode | int | None = None):
     """(y_re, y_im) = A v (kernels.hpp:399-416)."""
-    xr, xi = _aos(v_re, "spmv_complex"), _aos(v_im, "spmv_complex")
+    xr, xi = _aos(v_re, "spmv_complex", A.K), _aos(v_im, "spmv_complex", A.K)
     if xr.shape[0] != xi.shape[0]:
         raise ValueError("spmv_complex: re/im vector length mismatch")
     yr, yi = np.empty((A.nrows, A.K)), np.empty((A.nrows, A.K))
@@ -328,9 +333,7 @@ def sptmv(A: DeviceCsr, v, mode: KernelMode | int | None = None) -> np.ndarray:
     sptmv at ``mode.threads`` OpenMP threads (its per-thread accumulators are
     merged in thread order, so the bits depend on the thread count).  Needs
     ``DeviceCsr(..., transpose=True)``."""
-    x = _aos(v, "sptmv")
-    if x.shape[1] != A.K:
-        raise ValueError(f"sptmv: vector has K={x.shape[1]} components, matrix has K={A.K}")
+    x = _aos(v, "sptmv", A.K)
     y = np.empty((A.ncols, A.K))
     A.ctx.check(lib().mpsg_sptmv_ex(A.ctx.h, A.h, _order(mode), _threads(mode), x.shape[0], _p(x), _p(y)))
     return y
@@ -338,7 +341,7 @@ def sptmv(A: DeviceCsr, v, mode: KernelMode | int | None = None) -> np.ndarray:
 
 def sptmv_complex(A: DeviceCsr, v_re, v_im, mode: KernelMode | int | None = None, conjugate: bool = False):
     """(y_re, y_im) = A^T v, or the adjoint A^H v with ``conjugate`` (kernels.hpp:419-441)."""
-    xr, xi = _aos(v_re, "sptmv_complex"), _aos(v_im, "sptmv_complex")
+    xr, xi = _aos(v_re, "sptmv_complex", A.K), _aos(v_im, "sptmv_complex", A.K)
     if xr.shape[0] != xi.shape[0]:
         raise ValueError("sptmv_complex: re/im vector length mismatch")
     yr, yi = np.empty((A.ncols, A.K)), np.empty((A.ncols, A.K))
@@ -470,7 +473,7 @@ def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult
     cfg = cfg or SolverConfig()
     cfg.validate()
     A = op.matrix
-    bb = _aos(b, "solver")
+    bb = _aos(b, "solver", A.K)
     if op.rows() != op.cols():
         raise ValueError(f"solver: operator must be square, got {op.rows()}x{op.cols()}")
     if bb.shape[0] != op.cols():
@@ -501,7 +504,7 @@ def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult
 def _solve_method(op: CsrOperator, b, cfg: SolverConfig, method) -> SolveResult:
     cfg.validate()
     A = op.matrix
-    bb = _aos(b, "solver")
+    bb = _aos(b, "solver", A.K)
     if op.rows() != op.cols():
         raise ValueError(f"solver: operator must be square, got {op.rows()}x{op.cols()}")
     if bb.shape[0] != op.cols():
@@ -673,8 +676,8 @@ class DistCsr:
 
 def dspmv(A: DistCsr, x_local, mode: KernelMode | int | None = None) -> np.ndarray:
     """y_local = (A x)[this rank's rows]; x_local is this rank's block.  Collective."""
-    x = _aos(x_local, "spmv")
-    if x.shape[0] != A.row_end - A.row_begin or x.shape[1] != A.K:
+    x = _aos(x_local, "spmv", A.K)
+    if x.shape[0] != A.row_end - A.row_begin:
         raise ValueError(f"spmv: vector length {x.shape[0]} does not match the row block "
                          f"{A.row_end - A.row_begin}")
     y = np.empty((A.row_end - A.row_begin, A.K))
@@ -695,11 +698,13 @@ def dsolve_cg(A: DistCsr, b_local, cfg: SolverConfig | None = None) -> SolveResu
     """Row-sharded device CG; b_local / result x are this rank's blocks.  Collective."""
     cfg = cfg or SolverConfig()
     cfg.validate()
-    bb = _aos(b_local, "solver")
+    bb = _aos(b_local, "solver", A.K)
     if bb.shape[0] != A.row_end - A.row_begin:
         raise ValueError("solver: rhs length does not match the operator")
     x0 = None
     if cfg.x0 is not None and len(cfg.x0) > 0:
+        if len(cfg.x0) != A.nglobal:
+            raise ValueError("solver: x0 length does not match the rhs")
         x0 = np.zeros_like(bb)
         x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)[A.row_begin:A.row_end]
     c = _CgConfig(cfg.rel_tol, cfg.abs_tol, cfg.max_iters, cfg.check_every, 1 if cfg.use_graph else 0)
@@ -724,11 +729,13 @@ def dsolve(A: DistCsr, b_local, cfg: SolverConfig | None = None) -> SolveResult:
     every rank.  Collective."""
     cfg = cfg or SolverConfig()
     cfg.validate()
-    bb = _aos(b_local, "solver")
+    bb = _aos(b_local, "solver", A.K)
     if bb.shape[0] != A.row_end - A.row_begin:
         raise ValueError("solver: rhs length does not match the operator")
     x0 = None
     if cfg.x0 is not None and len(cfg.x0) > 0:
+        if len(cfg.x0) != A.nglobal:
+            raise ValueError("solver: x0 length does not match the rhs")
         x0 = np.zeros_like(bb)
         x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)[A.row_begin:A.row_end]
     c = _SolverConfig(int(cfg.method), max(cfg.threads, 1), cfg.rel_tol, cfg.abs_tol, cfg.max_iters,

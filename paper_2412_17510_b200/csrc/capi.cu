@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "internal.h"
 
 #include <omp.h>
@@ -273,17 +275,16 @@ bool can_overlap(const mpsg_ctx* ctx, const mpsg_csr* A) {
 }
 }  // namespace
 
-// ==========================================================================
-extern "C" {
+namespace {
+// Text of the last failed mpsg_ctx_create on this host thread (there is no
+// context to hang it on); read with mpsg_create_error().
+thread_local std::string g_create_err;
 
-const char* mpsg_version(void) { return "mpsg 0.1 (sm_100a)"; }
-
-int mpsg_ctx_create(int device, mpsg_ctx** out) {
-  if (!out) return MPSG_E_ARG;
-  *out = nullptr;
-  auto* ctx = new mpsg_ctx();
-  ctx->device = device;
+cudaError_t ctx_init(mpsg_ctx* ctx, int device) {
   cudaError_t e = cudaSetDevice(device);
+  // cudaSetDevice is lazy: force primary-context creation here so a busy or
+  // unusable device is reported by this call, not by the first launch
+  if (e == cudaSuccess) e = cudaFree(nullptr);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
@@ -294,8 +295,43 @@ int mpsg_ctx_create(int device, mpsg_ctx** out) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_side1, cudaEventDisableTiming);
   for (auto& ev : ctx->ev_part)
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  if (e != cudaSuccess) {
-    delete ctx;
+  return e;
+}
+}  // namespace
+
+// ==========================================================================
+extern "C" {
+
+const char* mpsg_version(void) { return "mpsg 0.1 (sm_100a)"; }
+
+const char* mpsg_create_error(void) { return g_create_err.c_str(); }
+
+// The one retry policy of the library (the C++ Context, the Python Context and
+// the CLI all come through here): a device that is momentarily held by another
+// process (cudaErrorDevicesUnavailable -- an exclusive-process GPU whose
+// previous owner is still tearing its context down) is retried for up to ~2 s;
+// every other error fails at once.  On failure everything created so far is
+// released and the CUDA error text is kept for mpsg_create_error().
+int mpsg_ctx_create(int device, mpsg_ctx** out) {
+  if (!out) return MPSG_E_ARG;
+  *out = nullptr;
+  g_create_err.clear();
+  mpsg_ctx* ctx = nullptr;
+  cudaError_t e = cudaSuccess;
+  for (int attempt = 0;; ++attempt) {
+    ctx = new mpsg_ctx();
+    ctx->device = device;
+    e = ctx_init(ctx, device);
+    if (e == cudaSuccess) break;
+    mpsg_ctx_destroy(ctx);
+    ctx = nullptr;
+    cudaGetLastError();
+    if (e != cudaErrorDevicesUnavailable || attempt >= 8) break;
+    usleep(250000);
+  }
+  if (!ctx) {
+    g_create_err = std::string("mpsg_ctx_create(device=") + std::to_string(device) + "): " +
+                   cudaGetErrorName(e) + ": " + cudaGetErrorString(e);
     return MPSG_E_CUDA;
   }
   ctx->stream = ctx->own_stream;

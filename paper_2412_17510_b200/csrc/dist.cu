@@ -68,26 +68,33 @@ namespace {
 // `pull(q, src)` enqueues this rank's copies out of rank q's buffer; then
 // every rank waits until all copies out of its own buffer are done before it
 // may overwrite it.
+// A failure on this rank never skips a barrier: the other ranks are already
+// inside the collective, so this rank goes through all three barriers and
+// returns its first error at the end (the others complete normally).
 template <class Pull>
 int local_collective(const mpsg_comm* c, const void* mine, cudaStream_t st, Pull pull) {
   LocalGroup* g = c->local;
   const int r = c->rank;
-  CUDA_TRY(c->ctx, cudaSetDevice(c->ctx->device));
+  int rc = MPSG_OK;
+  auto cu = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == MPSG_OK) rc = fail(c->ctx, MPSG_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  };
+  cu(cudaSetDevice(c->ctx->device), "cudaSetDevice");
   g->ptr[(size_t)r] = mine;
-  CUDA_TRY(c->ctx, cudaEventRecord(g->ready[(size_t)r], st));
+  cu(cudaEventRecord(g->ready[(size_t)r], st), "cudaEventRecord");
   g->barrier();
-  for (int q = 0; q < g->P; ++q) {
+  for (int q = 0; q < g->P && rc == MPSG_OK; ++q) {
     if (q == r) continue;
-    CUDA_TRY(c->ctx, cudaStreamWaitEvent(st, g->ready[(size_t)q], 0));
-    int rc = pull(q, g->ptr[(size_t)q]);
-    if (rc) return rc;
+    cu(cudaStreamWaitEvent(st, g->ready[(size_t)q], 0), "cudaStreamWaitEvent");
+    if (rc == MPSG_OK) rc = pull(q, g->ptr[(size_t)q]);
   }
-  CUDA_TRY(c->ctx, cudaEventRecord(g->consumed[(size_t)r], st));
+  // recorded even after a failure: the producers wait on it before reuse
+  cu(cudaEventRecord(g->consumed[(size_t)r], st), "cudaEventRecord");
   g->barrier();
   for (int q = 0; q < g->P; ++q)
-    if (q != r) CUDA_TRY(c->ctx, cudaStreamWaitEvent(st, g->consumed[(size_t)q], 0));
+    if (q != r) cu(cudaStreamWaitEvent(st, g->consumed[(size_t)q], 0), "cudaStreamWaitEvent");
   g->barrier();  // the events may be re-recorded by the next collective only now
-  return MPSG_OK;
+  return rc;
 }
 }  // namespace
 
@@ -340,27 +347,40 @@ int mpsg_dcsr_upload(mpsg_comm* c, int K, int is_complex, int64_t nglobal, int64
   A->nglobal = nglobal;
   A->row_begin = row_begin;
   A->row_end = row_end;
+  // Collective setup.  Every rank reaches both status exchanges below even if
+  // its own local work failed (a bad column index, OOM): the exchange carries
+  // a status word, so all ranks fail together instead of the healthy ones
+  // blocking forever in a collective the failed rank never enters.
   int rc = mpsg_csr_upload(ctx, K, is_complex, nloc, nglobal, indptr, indices, planes, &A->local);
-  if (rc) return rc;
   // the column interval this rank reads (its own block is always local)
   int64_t lo = row_begin, hi = row_end;
-  const int64_t nnz = indptr[nloc];
-  for (int64_t k = 0; k < nnz; ++k) {
-    lo = std::min(lo, indices[k]);
-    hi = std::max(hi, indices[k] + 1);
+  if (rc == MPSG_OK) {
+    const int64_t nnz = indptr[nloc];
+    for (int64_t k = 0; k < nnz; ++k) {
+      lo = std::min(lo, indices[k]);
+      hi = std::max(hi, indices[k] + 1);
+    }
   }
-  // every rank's row block and read interval (tiny allgather at setup)
+  // every rank's row block, read interval and status (tiny allgather at setup)
   const int P = c->nranks;
-  std::vector<int64_t> mine = {row_begin, row_end, lo, hi}, all((size_t)4 * P);
-  if ((rc = allgather_host(c, mine.data(), all.data(), 4))) return rc;
+  std::vector<int64_t> mine = {row_begin, row_end, lo, hi, (int64_t)rc}, all((size_t)5 * P);
+  const std::string local_err = rc ? ctx->err : std::string();
+  int grc = allgather_host(c, mine.data(), all.data(), 5);
+  if (grc) return grc;
+  for (int q = 0; q < P; ++q)
+    if (all[5 * q + 4] != MPSG_OK) {
+      if (q == c->rank) return fail(ctx, rc, "%s", local_err.c_str());
+      return fail(ctx, (int)all[5 * q + 4], "dcsr_upload: rank %d failed its local upload (status %lld)", q,
+                  (long long)all[5 * q + 4]);
+    }
   A->bounds.assign((size_t)P + 1, 0);
   A->need.assign((size_t)2 * P, 0);
   for (int q = 0; q < P; ++q) {
-    if (all[4 * q] != A->bounds[q])
+    if (all[5 * q] != A->bounds[q])
       return fail(ctx, MPSG_E_ARG, "dcsr_upload: row blocks are not contiguous in rank order");
-    A->bounds[q + 1] = all[4 * q + 1];
-    A->need[2 * q] = all[4 * q + 2];
-    A->need[2 * q + 1] = all[4 * q + 3];
+    A->bounds[q + 1] = all[5 * q + 1];
+    A->need[2 * q] = all[5 * q + 2];
+    A->need[2 * q + 1] = all[5 * q + 3];
   }
   if (A->bounds[P] != nglobal) return fail(ctx, MPSG_E_ARG, "dcsr_upload: row blocks do not cover the matrix");
   A->send.assign((size_t)2 * P, 0);
@@ -397,16 +417,27 @@ int mpsg_dcsr_upload(mpsg_comm* c, int K, int is_complex, int64_t nglobal, int64
         if (e) return e;
         return remap_rows(ctx, *out_csr, rows);
       };
-      if ((rc = sub(rint, &A->local_int))) return rc;
-      if ((rc = sub(rbnd, &A->local_bnd))) return rc;
+      rc = sub(rint, &A->local_int);
+      if (rc == MPSG_OK) rc = sub(rbnd, &A->local_bnd);
       A->n_interior = (int64_t)rint.size();
     }
   }
   const size_t xb = (size_t)std::max<int64_t>(nglobal, 1) * K * sizeof(double);
-  for (int j = 0; j < (A->cplx ? 2 : 1); ++j) {
-    CUDA_TRY(ctx, cudaMalloc(&A->xfull[j], xb));
-    CUDA_TRY(ctx, cudaMemset(A->xfull[j], 0, xb));
+  for (int j = 0; j < (A->cplx ? 2 : 1) && rc == MPSG_OK; ++j) {
+    cudaError_t e = cudaMalloc(&A->xfull[j], xb);
+    if (e == cudaSuccess) e = cudaMemset(A->xfull[j], 0, xb);
+    if (e != cudaSuccess) rc = fail(ctx, MPSG_E_CUDA, "dcsr_upload: %s", cudaGetErrorString(e));
   }
+  // second status exchange: the local work after the first one may have failed
+  std::vector<int64_t> st1 = {(int64_t)rc}, st_all((size_t)P);
+  const std::string local_err2 = rc ? ctx->err : std::string();
+  if ((grc = allgather_host(c, st1.data(), st_all.data(), 1))) return grc;
+  for (int q = 0; q < P; ++q)
+    if (st_all[(size_t)q] != MPSG_OK) {
+      if (q == c->rank) return fail(ctx, rc, "%s", local_err2.c_str());
+      return fail(ctx, (int)st_all[(size_t)q], "dcsr_upload: rank %d failed its local setup (status %lld)", q,
+                  (long long)st_all[(size_t)q]);
+    }
   *out = holder.release();
   return MPSG_OK;
 }

@@ -53,10 +53,13 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
                                : A->sell();
   if (part != -1 && S.nslices > 0) {
     const int blocks = (S.nslices + 3) / 4;
-    // Short rows: ORDER_FAST runs them in the reference's lanes-off order
-    // (bit-exact with lanes off, so trivially inside the fast-mode bound) --
-    // the faster of the two exact orders on B200 for every K
-    // (profiles/r01b_variants.txt); only long rows are reordered.
+    // Short rows: ORDER_FAST walks them in the reference's lanes-off element
+    // order (the faster of the two exact orders on B200 for every K,
+    // profiles/r01b_variants.txt) but, with MPSG_FUSED=1 (the default), each
+    // term goes through the fused product-accumulate fma_acc (mc_arith.cuh),
+    // so the bits differ from lanes off and the result is held to the
+    // componentwise bound instead; MPSG_FUSED=0 falls back to the exact
+    // lanes-off chain.
     const int sorder = order == ORDER_FAST ? ORDER_SCALAR : order;
     const bool seg = order == ORDER_SCALAR && ctx->seg_T > 1;
     if constexpr (!CPLX) {

@@ -17,11 +17,12 @@
 // With CONJ (the adjoint of sptmv_complex, kernels.hpp:419-441, run on the
 // transposed matrix) the combine is y.re = rr + ii, y.im = ri - ir.
 //
-// Fast mode (ORDER_FAST) runs short rows in the lanes-off order (exact) and
-// reorders long rows only: a row is cut into warp chunks, lanes accumulate
-// strided partials with the reference ops, a fixed shuffle tree and a fixed
-// chunk-order combine finish the row (deterministic, but not the reference
-// order; checked against the componentwise bound).
+// Fast mode (ORDER_FAST) walks short rows in the lanes-off element order with
+// the fused product-accumulate (fma_acc, one renormalisation sweep per
+// nonzero) and cuts long rows into warp chunks: lanes accumulate strided
+// partials, a fixed shuffle tree and a fixed chunk-order combine finish the
+// row (deterministic, but not the reference's bits; checked against the
+// componentwise bound).
 #pragma once
 
 #include "layout.h"

@@ -292,12 +292,12 @@ mpsg_csr* upload(mpsg_ctx* ctx, const Csr& A, int K, bool cplx, bool mixed, bool
 
 // Context creation, retried a few times: a device-initialisation failure can be
 // transient while another process on the GPU is tearing its context down.
-static bool open_ctx(int device, mpsg_ctx** ctx) {
-  for (int attempt = 0; attempt < 4; ++attempt) {
-    if (mpsg_ctx_create(device, ctx) == MPSG_OK) return true;
-    std::this_thread::sleep_for(std::chrono::milliseconds(250));
-  }
-  return false;
+// mpsg_ctx_create owns the retry policy (a device briefly held by another
+// process); anything it cannot recover from is reported with the CUDA text.
+static mpsg_ctx* open_ctx(int device) {
+  mpsg_ctx* ctx = nullptr;
+  if (mpsg_ctx_create(device, &ctx) != MPSG_OK) die(std::string("no usable sm_100a GPU: ") + mpsg_create_error(), 1);
+  return ctx;
 }
 
 int run_spmv(const Args& a) {
@@ -308,8 +308,7 @@ int run_spmv(const Args& a) {
   const bool mixed = a.mode == "m", cplx = coo.complex;
   const int order = order_of(a.lanes);
   if (a.reps < 1) die("time_kernel: repetitions must be at least 1");
-  mpsg_ctx* ctx = nullptr;
-  if (!open_ctx(a.device, &ctx)) die("no usable sm_100a GPU", 1);
+  mpsg_ctx* ctx = open_ctx(a.device);
   mpsg_csr* d = upload(ctx, A, K, cplx, mixed, a.transposed);
   const int64_t n = A.ncols;
   std::vector<double> vr((size_t)n * K), vi(cplx ? (size_t)n * K : 0), yr((size_t)n * K), yi(vi.size());
@@ -362,8 +361,7 @@ int run_solve(const Args& a) {
   const Csr A = coo_to_csr(coo);
   if (A.nrows != A.ncols) die("solve: the matrix must be square", 1);
   const int K = precision_k(a.precision);
-  mpsg_ctx* ctx = nullptr;
-  if (!open_ctx(a.device, &ctx)) die("no usable sm_100a GPU", 1);
+  mpsg_ctx* ctx = open_ctx(a.device);
   mpsg_csr* d = upload(ctx, A, K, false, mixed, method == MPSG_BICG);
   const int64_t n = A.ncols;
   const int threads = a.threads > 0 ? a.threads : 1;

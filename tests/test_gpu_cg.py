@@ -108,10 +108,13 @@ def test_cg_config_errors(ctx):
         M.solve_cg(M.CsrOperator(M.DeviceCsr(R, 2, ctx=ctx)), b)
 
 
+@pytest.mark.parametrize("fast", [False, True], ids=["lane4", "fast"])
 @pytest.mark.parametrize("K", [2, 4])
-def test_cg_full_config5_500_iterations(ctx, K):
+def test_cg_full_config5_500_iterations(ctx, K, fast):
     """Config 5 (3D 7-pt Laplacian 128^3 + 1e-3 shift), 500 iterations: the GPU
-    reaches the reference's final residual within 500 +- 5 iterations."""
+    reaches the reference's final residual within 500 +- 5 iterations -- in the
+    bit-exact LANE4 order and in the FAST order bench.py times (fused
+    product-accumulates in the SpMV and the CG vector kernels, tree dots)."""
     try:
         g = golden("cg_full")
     except FileNotFoundError:
@@ -122,7 +125,7 @@ def test_cg_full_config5_500_iterations(ctx, K):
     b = M.spmv(dA, xt, M.ORDER_LANE4)
     assert M.checksum(b) == int(g[f"cg5_K{K}_b_checksum"])
     ref_h = g[f"cg5_K{K}_history"]
-    res = M.solve_cg(M.CsrOperator(dA), b, M.SolverConfig(rel_tol=1e-30, max_iters=510))
+    res = M.solve_cg(M.CsrOperator(dA), b, M.SolverConfig(rel_tol=1e-30, max_iters=510, fast=fast))
     h = np.asarray(res.report.residual_history)
     target = ref_h[500]
     k = _iters_to_reach(h, target)

@@ -257,3 +257,40 @@ def test_dsolve_rejects_bicg(ctx):
         M.dsolve(dA, b, M.SolverConfig(method=M.KrylovMethod.BiCG))
     dA.close()
     comm.close()
+
+
+@pytest.mark.parametrize("P,bad", [(2, 0), (3, 1), (3, 2)])
+def test_failing_rank_fails_every_rank_without_hanging(P, bad):
+    """One rank's local upload fails (a column index out of range): every rank
+    gets an error from the collective setup instead of blocking in it."""
+    import threading
+
+    A = synth.config_matrix(5, 2, 10)
+    bounds = M.partition_rows(A.indptr, A.nrows, P)
+    ctxs = [M.Context(0) for _ in range(P)]
+    comms = M.Comm.local_group(ctxs)
+    errs = [None] * P
+
+    def body(r):
+        Al = M.shard_rows(A, int(bounds[r]), int(bounds[r + 1]))
+        if r == bad:
+            Al.indices = Al.indices.copy()
+            Al.indices[0] = A.nrows + 7  # out of range
+        try:
+            d = M.DistCsr(comms[r], Al, 2, A.nrows, int(bounds[r]), int(bounds[r + 1]))
+            d.close()
+        except Exception as e:  # noqa: BLE001
+            errs[r] = str(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in ts), "a rank hung in the setup collective"
+    assert all(e is not None for e in errs), errs
+    assert f"rank {bad} failed" in errs[(bad + 1) % P]
+    for c in comms:
+        c.close()
+    for c in ctxs:
+        c.close()

@@ -55,10 +55,29 @@ def test_fast_wide_exponent_range(ctx, K):
 
 @pytest.mark.parametrize("K", [2, 3, 4])
 def test_fast_exact_cancellation(ctx, K):
+    """Adjacent a / -a pairs times a CONSTANT x, so the running accumulator
+    really cancels: exactly (whole pairs), down to a level-1 residue (the
+    pair agrees in its leading component only) and down to a level-2 residue
+    (leading two agree).  The fused accumulate then runs with s0 ~ 0 and its
+    non-canonical accumulator fed back in -- the case where the level-wise
+    quick-two-sums see |h| > |s0|."""
+    rng = np.random.default_rng(100 + K)
     A = synth.config_matrix(2, K, 20000, 40.0)
-    A.planes[:, 1::2] = -A.planes[:, 0::2][:, : A.planes[:, 1::2].shape[1]]
-    x = synth.config_vector(2, A.nrows, K)
-    _check(A, x, M.spmv(M.DeviceCsr(A, K, ctx=ctx), x, M.ORDER_FAST), K)
+    P = A.planes
+    m = P[:, 1::2].shape[1]
+    P[:, 1::2] = -P[:, 0::2][:, :m]
+    kind = rng.integers(0, 3, m)  # 0: exact, 1: level-1 residue, 2: level-2 residue
+    for lev in (1, 2):
+        if lev >= K:
+            continue
+        sel = np.nonzero(kind == lev)[0]
+        fresh = synth.vector(synth.VAL_NORMAL, len(sel), K, seed=7 + lev).T  # (K, len)
+        for j in range(lev, K):
+            P[j, 1 + 2 * sel] = fresh[j] * np.abs(P[lev - 1, 1 + 2 * sel]) * 2.0 ** (-53 * (j - lev + 1))
+    x1 = synth.config_vector(2, 1, K)[0]
+    x = np.tile(x1, (A.nrows, 1))
+    w = _check(A, x, M.spmv(M.DeviceCsr(A, K, ctx=ctx), x, M.ORDER_FAST), K)
+    assert np.isfinite(w)
 
 
 @pytest.mark.parametrize("K", [3, 4])
