@@ -734,6 +734,24 @@ MPSG_DI int ld_s32_stream(const int* q) {
 #endif
 }
 
+MPSG_DI void ld_v4(const double* q, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(q));
+}
+// QD gather of x[i] as one 256-bit load (LDG.E.ENL2.256, sm_100; the caller
+// guarantees p is 32-byte aligned) instead of two 128-bit ones: one L1
+// wavefront per random gather instead of two.  The x gathers dominate the L1
+// request load of the real SELL kernels (cfg2 QD ncu: L1/TEX 81% -> 57% busy,
+// +2.3%).  A TD variant (the 24-byte element read from its aligned 32-byte
+// window, or from two windows when it straddles) measured slower than three
+// 64-bit loads (cfg2 TD 126.0 -> 123.0 Gnnz/s) and was dropped.
+template <int K>
+MPSG_DI MC<K> load_x_wide(const double* __restrict__ p, int64_t i) {
+  static_assert(K == 4, "256-bit gathers are used for QD only");
+  MC<K> r;
+  ld_v4(p + 4 * i, r.c[0], r.c[1], r.c[2], r.c[3]);
+  return r;
+}
+
 template <int K>
 MPSG_DI MC<K> load_aos(const double* __restrict__ p, int64_t i) {
   MC<K> r;

@@ -51,6 +51,10 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
   }
   const SellView S = part >= 0 ? A->sell_range(A->part_slice[(size_t)part], A->part_slice[(size_t)part + 1])
                                : A->sell();
+  // 256-bit x gathers (QD real kernels) need a 32-byte aligned x.  TD keeps
+  // its three 64-bit loads: the windowed 256-bit TD gather (load_x_wide<3>)
+  // measured slower (cfg2 TD 126.0 -> 123.0, cfg5 TD 134.3 -> 121.7 Gnnz/s).
+  const bool xw = K == 4 && (reinterpret_cast<uintptr_t>(xre) & 31) == 0;
   if (part != -1 && S.nslices > 0) {
     const int blocks = (S.nslices + 3) / 4;
     // Short rows: ORDER_FAST walks them in the reference's lanes-off element
@@ -66,16 +70,22 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
       if (seg)
         sell_real_seg_kernel<K, MX><<<blocks, 128, 0, st>>>(S, xre, yre, ctx->seg_bounds, ctx->seg_T);
       else if (order == ORDER_FAST && MPSG_FUSED)
-        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_FAST, MX>, blocks, 128, 0, st, xre, xb, S, xre,
-                                 yre));
+        CUDA_TRY(ctx, xw ? launch_win(ctx, sell_real_kernel<K, ORDER_FAST, MX, K == 4>, blocks, 128, 0, st, xre, xb, S,
+                                      xre, yre)
+                         : launch_win(ctx, sell_real_kernel<K, ORDER_FAST, MX, false>, blocks, 128, 0, st, xre, xb,
+                                      S, xre, yre));
       else if (sorder == ORDER_SCALAR)
-        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_SCALAR, MX>, blocks, 128, 0, st, xre, xb, S, xre,
-                                 yre));
+        CUDA_TRY(ctx, xw ? launch_win(ctx, sell_real_kernel<K, ORDER_SCALAR, MX, K == 4>, blocks, 128, 0, st, xre, xb,
+                                      S, xre, yre)
+                         : launch_win(ctx, sell_real_kernel<K, ORDER_SCALAR, MX, false>, blocks, 128, 0, st, xre, xb,
+                                      S, xre, yre));
       else if constexpr (K == 2)
         CUDA_TRY(ctx, launch_win(ctx, sell_real_lane4_lat_kernel<K, MX>, blocks, 128, 0, st, xre, xb, S, xre, yre));
       else
-        CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_LANE4, MX>, blocks, 128, 0, st, xre, xb, S, xre,
-                                 yre));
+        CUDA_TRY(ctx, xw ? launch_win(ctx, sell_real_kernel<K, ORDER_LANE4, MX, K == 4>, blocks, 128, 0, st, xre, xb,
+                                      S, xre, yre)
+                         : launch_win(ctx, sell_real_kernel<K, ORDER_LANE4, MX, false>, blocks, 128, 0, st, xre, xb,
+                                      S, xre, yre));
     } else {
       if (seg)
         sell_complex_kernel<K, ORDER_SCALAR, MX, CONJ, true>

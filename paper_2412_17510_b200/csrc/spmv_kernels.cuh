@@ -100,14 +100,25 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 #define MPSG_FUSED_G_QD 4
 #endif
 
+// x gather in the real SELL kernels: QD with one 256-bit load when x is
+// 32-byte aligned (the kernel's XW flag, checked per launch), else the plain
+// AoS loads.
+template <int K>
+MPSG_DI MC<K> load_x(const double* __restrict__ x, bool xw, int64_t i) {
+  if constexpr (K == 4) {
+    if (xw) return load_x_wide<K>(x, i);
+  }
+  return load_aos<K>(x, i);
+}
+
 // Product term of slot-row element k.
 template <int K, bool MX>
 MPSG_DI MC<K> sell_term(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
-                        const double* __restrict__ x, int k) {
+                        const double* __restrict__ x, bool xw, int k) {
   const int64_t e = (int64_t)k * 32;
   AVal<K, MX> a;
   a.load(vp, st, e);
-  return a.times(load_aos<K>(x, ld_s32_stream(cp + e)));
+  return a.times(load_x<K>(x, xw, ld_s32_stream(cp + e)));
 }
 
 // LANE4 order with the four lane chains evaluated P at a time.  Chain j
@@ -120,7 +131,7 @@ MPSG_DI MC<K> sell_term(const double* __restrict__ vp, const int* __restrict__ c
 // measured in profiles/r01b_variants.txt.
 template <int K, bool MX>
 MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
-                        const double* __restrict__ x, int len) {
+                        const double* __restrict__ x, bool xw, int len) {
   constexpr int P = K == 2 ? 2 : 1;
   const int nfull = len >> 2;
   MC<K> s = zero<K>();
@@ -137,19 +148,19 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
         const int cn = (m + 1 < nfull) ? ld_s32_stream(cp + (int64_t)(e + 4) * 32) : 0;
         AVal<K, MX> a;
         a.load(vp, st, (int64_t)e * 32);
-        L[0] = add(L[0], a.times(load_aos<K>(x, c)));
+        L[0] = add(L[0], a.times(load_x<K>(x, xw, c)));
         c = cn;
       }
     } else {
       for (int m = 0; m < nfull; ++m) {
 #pragma unroll
-        for (int c = 0; c < P; ++c) L[c] = add(L[c], sell_term<K, MX>(vp, cp, st, x, 4 * m + j0 + c));
+        for (int c = 0; c < P; ++c) L[c] = add(L[c], sell_term<K, MX>(vp, cp, st, x, xw, 4 * m + j0 + c));
       }
     }
 #pragma unroll
     for (int c = 0; c < P; ++c) s = add(s, L[c]);
   }
-  for (int k = nfull * 4; k < len; ++k) s = add(s, sell_term<K, MX>(vp, cp, st, x, k));
+  for (int k = nfull * 4; k < len; ++k) s = add(s, sell_term<K, MX>(vp, cp, st, x, xw, k));
   return s;
 }
 
@@ -160,7 +171,7 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
 // no prefetch (occupancy-bound); TD/QD: G = 2 with prefetch (64 registers).
 template <int K, bool MX, bool FUSED = false>
 MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
-                         const double* __restrict__ x, int len) {
+                         const double* __restrict__ x, bool xw, int len) {
   constexpr int G = K == 2 ? 4 : (FUSED ? (K == 4 ? MPSG_FUSED_G_QD : 2) : 2);
   constexpr bool PF = K != 2;
   MC<K> acc = zero<K>();
@@ -179,7 +190,7 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
 #pragma unroll
         for (int j = 0; j < G; ++j) {
           a[j].load(vp, st, (int64_t)(k + j) * 32);
-          v[j] = load_aos<K>(x, c[j]);
+          v[j] = load_x<K>(x, xw, c[j]);
         }
 #pragma unroll
         for (int j = 0; j < G; ++j) acc = a[j].accumulate(acc, v[j]);
@@ -189,7 +200,7 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
         for (int j = 0; j < G; ++j) {
           AVal<K, MX> a;
           a.load(vp, st, (int64_t)(k + j) * 32);
-          p[j] = a.times(load_aos<K>(x, c[j]));
+          p[j] = a.times(load_x<K>(x, xw, c[j]));
         }
 #pragma unroll
         for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
@@ -205,9 +216,9 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
         AVal<K, MX> a;
         a.load(vp, st, (int64_t)(k + j) * 32);
         if constexpr (FUSED)
-          acc = a.accumulate(acc, load_aos<K>(x, c[j]));
+          acc = a.accumulate(acc, load_x<K>(x, xw, c[j]));
         else
-          acc = add(acc, a.times(load_aos<K>(x, c[j])));
+          acc = add(acc, a.times(load_x<K>(x, xw, c[j])));
       }
     if constexpr (FUSED) acc = canon(acc);
     return acc;
@@ -215,11 +226,11 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
     for (; k + G <= len; k += G) {
       MC<K> p[G];
 #pragma unroll
-      for (int j = 0; j < G; ++j) p[j] = sell_term<K, MX>(vp, cp, st, x, k + j);
+      for (int j = 0; j < G; ++j) p[j] = sell_term<K, MX>(vp, cp, st, x, xw, k + j);
 #pragma unroll
       for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
     }
-    for (; k < len; ++k) acc = add(acc, sell_term<K, MX>(vp, cp, st, x, k));
+    for (; k < len; ++k) acc = add(acc, sell_term<K, MX>(vp, cp, st, x, xw, k));
     return acc;
   }
 }
@@ -262,7 +273,7 @@ struct SegFold {
 // ---------------------------------------------------------------------------
 // Row sum of slot `lane` of SELL slice s in the chosen order; row = the
 // original row (-1 for padding).
-template <int K, int ORDER, bool MX>
+template <int K, int ORDER, bool MX, bool XW>
 MPSG_DI MC<K> sell_row(const SellView& S, const double* __restrict__ x, int s, int lane, int& row) {
   const int slot = s * 32 + lane;
   row = S.slot_row[slot];
@@ -270,33 +281,36 @@ MPSG_DI MC<K> sell_row(const SellView& S, const double* __restrict__ x, int s, i
   const int64_t base = S.slice_ptr[s] + lane;
   const int* __restrict__ cp = S.col + base;
   const double* __restrict__ vp = S.val + base;
+  constexpr bool xw = XW;
   if constexpr (ORDER == ORDER_SCALAR)
-    return scalar_row<K, MX>(vp, cp, S.stride, x, len);
+    return scalar_row<K, MX>(vp, cp, S.stride, x, xw, len);
   else if constexpr (ORDER == ORDER_FAST)
-    return scalar_row<K, MX, true>(vp, cp, S.stride, x, len);  // fused multiply-accumulate (TD/QD)
+    return scalar_row<K, MX, true>(vp, cp, S.stride, x, xw, len);  // fused multiply-accumulate (TD/QD)
   else
-    return lane4_row<K, MX>(vp, cp, S.stride, x, len);
+    return lane4_row<K, MX>(vp, cp, S.stride, x, xw, len);
 }
 
-template <int K, int ORDER, bool MX>
+// XW: x is 32-byte aligned and gathered with 256-bit loads (load_x_wide);
+// the launcher checks the alignment of each call's x.
+template <int K, int ORDER, bool MX, bool XW>
 MPSG_DI void sell_real_body(const SellView& S, const double* __restrict__ x, double* __restrict__ y) {
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= S.nslices) return;
   int row;
-  const MC<K> acc = sell_row<K, ORDER, MX>(S, x, s, threadIdx.x & 31, row);
+  const MC<K> acc = sell_row<K, ORDER, MX, XW>(S, x, s, threadIdx.x & 31, row);
   if (row >= 0) store_aos<K>(y, row, acc);
 }
 
-template <int K, int ORDER, bool MX>
+template <int K, int ORDER, bool MX, bool XW>
 __global__ void MPSG_SELL_LB sell_real_kernel(SellView S, const double* __restrict__ x, double* __restrict__ y) {
-  sell_real_body<K, ORDER, MX>(S, x, y);
+  sell_real_body<K, ORDER, MX, XW>(S, x, y);
 }
 // DD in the LANE4 order is memory-latency-bound: capped at 40 registers for
 // 12 resident blocks per SM (measured +17% on config 5, profiles/r01b_*).
 template <int K, bool MX>
 __global__ void __launch_bounds__(128, 12) sell_real_lane4_lat_kernel(SellView S, const double* __restrict__ x,
                                                                      double* __restrict__ y) {
-  sell_real_body<K, ORDER_LANE4, MX>(S, x, y);
+  sell_real_body<K, ORDER_LANE4, MX, false>(S, x, y);
 }
 
 // Transposed product at T > 1 threads, real (see SegFold).

@@ -260,3 +260,27 @@ def test_host_call_overlapped_parts(K, order):
         rr, ri = O.spmv_complex(A, xr, xi, order)
         assert bits_equal(yr, rr) and bits_equal(yi, ri)
     c.close()
+
+
+@pytest.mark.parametrize("order", [0, 1, 2])
+def test_unaligned_device_x_takes_the_narrow_gather(order):
+    """QD x gathers use 256-bit loads only when x is 32-byte aligned; an x
+    that starts 8 bytes into an allocation must give the same result."""
+    import torch
+
+    c = M.Context(0)
+    K = 4
+    A = synth.config_matrix(2, K, 3000)
+    x = synth.config_vector(2, A.nrows, K)
+    dA = M.DeviceCsr(A, K, ctx=c)
+    flat = torch.zeros(A.nrows * K + 1, dtype=torch.float64, device="cuda")
+    flat[1:] = torch.from_numpy(x.reshape(-1)).cuda()
+    assert (flat.data_ptr() + 8) % 32 != 0
+    dy = torch.empty((A.nrows, K), dtype=torch.float64, device="cuda")
+    M.spmv_dev(dA, flat.data_ptr() + 8, dy.data_ptr(), order, None)
+    c.synchronize()
+    aligned = M.spmv(dA, x, order)
+    assert bits_equal(dy.cpu().numpy(), aligned)
+    if order != 2:
+        assert bits_equal(aligned, O.spmv(A, x, order))
+    c.close()
