@@ -66,6 +66,7 @@ OPS_FAST_MIXED = {2: 17, 3: 114, 4: 76}
 OPS_FAST_UPDATE = {2: 20, 3: 68, 4: 143}
 ROW_CANON = {2: 0, 3: 16, 4: 22}
 K_NAME = {2: "DD", 3: "TD", 4: "QD"}
+ORDER_NAME = {0: "scalar", 1: "lane4", 2: "fast"}
 CG_ITERS = 500
 
 
@@ -282,7 +283,7 @@ def cpu_model() -> str:
         return "unknown"
 
 
-def best_reference(steps, warmup, cfg, K):
+def best_reference(steps, warmup, cfg, K, light=False):
     """The fastest way the reference computes this SpMV on this host: lanes on
     (its default) and off, its own flags and the x86-64-v3 build (all
     bit-identical), every host thread.  Each combination is screened with
@@ -300,7 +301,7 @@ def best_reference(steps, warmup, cfg, K):
         O.use_ref_build(v3)
         try:
             for order in (1, 0):
-                r = run_reference(2, 1, cfg, K, order=order, inputs=inputs)
+                r = run_reference(1 if light else 2, 1, cfg, K, order=order, inputs=inputs)
                 label = f"{'x86-64-v3 build' if v3 else 'reference flags'}, lanes {'on' if order else 'off'}, " \
                         f"threads={r['cores']}"
                 rows[label] = r["value"]
@@ -308,7 +309,8 @@ def best_reference(steps, warmup, cfg, K):
                     best = (r["value"], v3, order, label)
         finally:
             O.use_ref_build(False)
-    rows["reference flags, lanes on, threads=1"] = run_reference(2, 1, cfg, K, threads=1, inputs=inputs)["value"]
+    rows["reference flags, lanes on, threads=1"] = run_reference(1 if light else 2, 0 if light else 1, cfg, K,
+                                                                 threads=1, inputs=inputs)["value"]
     _, v3, order, label = best
     O.use_ref_build(v3)
     try:
@@ -416,7 +418,7 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant="pure"):
     t_total = max_over_ranks(torch, dev, dist, sum(ms) / 1e3)
 
     # e2e through the host-pointer C-ABI call (pinned host buffers, H2D + D2H inside)
-    e2e = None
+    e2e = e2e_pageable = None
     if not args.no_e2e and not shard and variant == "pure":
         if cplx:
             hx = [torch.from_numpy(v).pin_memory() for v in xs]
@@ -445,7 +447,31 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant="pure"):
             ets.append(e0.elapsed_time(e1) / 1e3)
         te = max_over_ranks(torch, dev, dist, sum(ets))
         e2e = {"value": world * nnz * args.steps / te / 1e9, "unit": "Gnnz/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "call": "mpsg_spmv_complex" if cplx else "mpsg_spmv"}
+               "d2h_bytes_per_step": d2h, "call": "mpsg_spmv_complex" if cplx else "mpsg_spmv",
+               "host_memory": "pinned"}
+        # the same call on pageable host arrays (numpy, like the drop-in's
+        # std::vector): the library stages them through its own pinned chunks
+        if cplx:
+            px = [np.ascontiguousarray(v) for v in xs]
+            py = [np.empty((n, K)) for _ in range(2)]
+            pcall = lambda: M.lib().mpsg_spmv_complex(ctx.h, dA.h, order, n, px[0].ctypes.data, px[1].ctypes.data,  # noqa
+                                                      py[0].ctypes.data, py[1].ctypes.data)
+        else:
+            px, py = np.ascontiguousarray(x), np.empty((n, K))
+            pcall = lambda: M.lib().mpsg_spmv(ctx.h, dA.h, order, n, px.ctypes.data, py.ctypes.data)  # noqa: E731
+        ctx.check(pcall())
+        pts = []
+        for _ in range(args.steps):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.check(pcall())
+            e1.record(stream)
+            torch.cuda.synchronize()
+            pts.append(e0.elapsed_time(e1) / 1e3)
+        tp = max_over_ranks(torch, dev, dist, sum(pts))
+        e2e_pageable = {"value": world * nnz * args.steps / tp / 1e9, "unit": "Gnnz/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "call": e2e["call"], "host_memory": "pageable (numpy)"}
     if local_stats is not None:
         kernels = (1 if local_stats.nslices > 0 else 0) + (1 if local_stats.nlong > 0 else 0)
     else:
@@ -467,8 +493,8 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant="pure"):
         l2_warm = {"value": nnz / tw / 1e9, "unit": "Gnnz/s", "us_per_step": tw * 1e6,
                    "note": f"{reps} back-to-back launches, L2 not flushed (working set fits in L2)"}
     res = dict(n=n, nnz=nnz, units=units, t_total=t_total, per_launch=t_total / args.steps, clocks=clocks,
-               e2e=e2e, launches=args.steps * kernels, cplx=cplx, halo_rows=halo, shard=shard, variant=variant,
-               l2_warm=l2_warm)
+               e2e=e2e, e2e_pageable=e2e_pageable, launches=args.steps * kernels, cplx=cplx, halo_rows=halo,
+               shard=shard, variant=variant, l2_warm=l2_warm, order=order)
     del dA
     if comm:
         comm.close()
@@ -654,34 +680,39 @@ def main():
     fp64_peak = M.measure_fp64_peak(probe)
     probe.close()
 
-    jobs = [(args.config, args.K, args.solver or args.cg, args.variant)]
+    jobs = [(args.config, args.K, args.solver or args.cg, args.variant, order)]
     if args.all:
-        jobs = [("cfg1", 2, False, "pure"), ("cfg2", 3, False, "pure"), ("cfg2", 4, False, "pure"),
-                ("cfg3", 2, False, "pure"), ("cfg3", 4, False, "pure"), ("cfg4", 2, False, "pure"),
-                ("cfg5", 2, False, "pure"), ("cfg5", 4, False, "pure"), ("cfg5", 2, True, "pure"),
-                ("cfg5", 4, True, "pure"), ("cfg2", 4, False, "mixed"), ("cfg4", 2, False, "mixed"),
-                ("cfg3", 4, False, "mixed"), ("cfg2", 4, False, "sptmv"), ("cfg3", 2, False, "sptmv"),
-                ("cfg5", 2, "bicgstab", "pure"), ("cfg5", 4, "bicgstab", "pure")]
+        spmv = [("cfg1", 2), ("cfg2", 3), ("cfg2", 4), ("cfg3", 2), ("cfg3", 4), ("cfg4", 2), ("cfg5", 2), ("cfg5", 4)]
+        jobs = [(c, k, False, "pure", order) for c, k in spmv]
+        jobs += [("cfg5", 2, True, "pure", order), ("cfg5", 4, True, "pure", order),
+                 ("cfg2", 4, False, "mixed", order), ("cfg4", 2, False, "mixed", order),
+                 ("cfg3", 4, False, "mixed", order), ("cfg2", 4, False, "sptmv", order),
+                 ("cfg3", 2, False, "sptmv", order), ("cfg5", 2, "bicgstab", "pure", order),
+                 ("cfg5", 4, "bicgstab", "pure", order)]
+        if order != 1:  # the bit-exact LANE4 order (the reference default, kernels.hpp:44) per SpMV config
+            jobs += [(c, k, False, "pure", 1) for c, k in spmv]
     secondary = None
     if (not args.all and args.config == "cfg2" and args.K == 4 and not args.cg and args.variant == "pure"
             and args.secondary != "none"):
-        secondary = ("cfg2", 3, False, "pure")
+        secondary = ("cfg2", 3, False, "pure", order)
 
     results = []
-    for cfg, K, cg, variant in jobs + ([secondary] if secondary else []):
+    for cfg, K, cg, variant, jorder in jobs + ([secondary] if secondary else []):
         if cg:
             meth = cg if isinstance(cg, str) else "cg"
-            r = run_gpu_cg(args, K, order, rank, world, dist, meth)
+            r = run_gpu_cg(args, K, jorder, rank, world, dist, meth)
             r["variant"] = "pure"
+            r["order"] = jorder
             r["roof"] = roofline(meth, r["nnz"], r["n"], K, False, r["per_iter"], hbm_peak, fp64_peak,
-                                 f"cg5_K{K}" if meth == "cg" else f"{meth}5_K{K}", fast=order == 2)
+                                 f"cg5_K{K}" if meth == "cg" else f"{meth}5_K{K}", fast=jorder == 2)
         else:
-            r = run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant)
-            tkey = f"{cfg}_K{K}" + ("" if variant == "pure" else f"_{variant}")
+            r = run_gpu_spmv(args, cfg, K, jorder, rank, world, dist, variant)
+            tkey = f"{cfg}_K{K}" + ("" if variant == "pure" else f"_{variant}") + ("" if jorder == 2 else f"_o{jorder}")
             r["roof"] = roofline("spmv", r["nnz"], r["n"], K, r["cplx"], r["per_launch"], hbm_peak, fp64_peak,
-                                 tkey, mixed=variant == "mixed", fast=order == 2)
+                                 tkey, mixed=variant == "mixed", fast=jorder == 2)
         results.append((cfg, K, cg, r))
 
+    cpu_cache = {}
     if rank == 0:
         for idx, (cfg, K, cg, r) in enumerate(results[: len(jobs)]):
             vname = {"pure": "", "mixed": " Mixed (binary64 matrix)", "sptmv": " SpTMV y=A^T x"}[r["variant"]]
@@ -700,11 +731,14 @@ def main():
                     "config": {"workload": f"{cfg} {K_NAME[K]}"
                                            f"{(' ' + r['method'].upper() + ' x' + str(r['iters'])) if cg else ''}"
                                            f"{vname}: {CONFIG_DESC[cfg]}",
-                               "precision": K_NAME[K], "order": args.order, "nnz": r["nnz"], "n": r["n"],
+                               "precision": K_NAME[K], "order": ORDER_NAME[r["order"]], "nnz": r["nnz"],
+                               "n": r["n"],
                                "parallelism": par,
                                "l2": ("flushed before every timed step: 256 MB write, then 256 MB read of a "
                                       "second buffer") if not cg else "inputs (A, vectors) larger than L2"},
                     "roofline": r["roof"], "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["launches"]}
+            if r.get("e2e_pageable"):
+                line["e2e_pageable"] = r["e2e_pageable"]
             if cg:
                 line["config"].update(step=f"one {r['iters']}-iteration {r['method']} solve (graph-captured "
                                            "batches of 32)",
@@ -720,15 +754,20 @@ def main():
                 line["secondary"] = {"workload": f"{c2} {K_NAME[k2]}",
                                      "value": r2["units"] * args.steps / r2["t_total"] / 1e9,
                                      "unit": "Gnnz/s", "roofline": r2["roof"], "e2e": r2["e2e"]}
-            if world == 1 and not args.no_cpu and not args.all and r["variant"] == "pure":
-                if cg:
-                    cb = run_reference(1, 0, cfg, K, cg=cg)
-                else:
-                    cb, cvar = best_reference(5, 1, cfg, K)
-                    if cvar:
-                        line["cpu_variants"] = cvar
+            if world == 1 and not args.no_cpu and r["variant"] == "pure" and (not args.all or not cg):
+                key = (cfg, K, cg)
+                if key not in cpu_cache:
+                    if cg:
+                        cpu_cache[key] = (run_reference(1, 0, cfg, K, cg=cg), None)
+                    else:  # --all: a lighter screen (1 timed call per variant) keeps the run to minutes
+                        cpu_cache[key] = best_reference(2 if args.all else 5, 1, cfg, K, light=args.all)
+                cb, cvar = cpu_cache[key]
+                if cvar:
+                    line["cpu_variants"] = cvar
                 line["cpu_baseline"] = {"value": cb["value"], "unit": "Gnnz/s", "cores": cb["cores"],
                                         "kind": cb["kind"], "sample": cb["sample"]}
+                if cvar and "reference flags, lanes on, threads=1" in cvar["rows"]:
+                    line["cpu_baseline"]["one_thread"] = cvar["rows"]["reference flags, lanes on, threads=1"]
             print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -3,7 +3,7 @@
 
     MPSG_LIB=/path/variant.so python tools/kbench.py cfg2:4:2 cfg2:3:2 cfg4:2:2 ...
 
-Each spec is cfg:K:order.  Times mpsg_spmv_dev with CUDA events on a private
+Each spec is cfg:K:order[:variant] (variant: pure | mixed | sptmv).  Times mpsg_spmv_dev with CUDA events on a private
 stream, L2 flushed (256 MB write + 256 MB read of a second buffer) before
 every timed launch, median of --steps launches; prints one line per spec.
 """
@@ -11,6 +11,8 @@ import argparse
 import os
 import statistics
 import sys
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -42,25 +44,37 @@ def main():
     libcuda = ctypes.CDLL("libcuda.so.1")  # demote persisting L2 lines before each flush
     cache = {}
     for spec in args.specs:
-        cfg, K, order = spec.split(":")
+        parts = spec.split(":")
+        cfg, K, order = parts[:3]
+        variant = parts[3] if len(parts) > 3 else "pure"  # pure | mixed | sptmv
         c, K, order = int(cfg[3]), int(K), int(order)
-        key = (c, K)
+        key = (c, K, variant)
         if key not in cache:
             cache.clear()
             A = synth.config_matrix(c, K)
             x = synth.config_vector(c, A.nrows, K)
-            cache[key] = (A, x, M.DeviceCsr(A, K, c == 3, ctx=ctx))
+            if variant == "mixed":  # the binary64 matrix: leading plane(s)
+                A.planes = np.ascontiguousarray(np.stack([A.planes[0], A.planes[K]]) if c == 3 else A.planes[:1])
+            cache[key] = (A, x, M.DeviceCsr(A, K, c == 3, ctx=ctx, mixed=variant == "mixed",
+                                            transpose=variant == "sptmv"))
         A, x, dA = cache[key]
         n = A.nrows
         if c == 3:
             xs = [torch.from_numpy(v).to(dev) for v in x]
             ys = [torch.empty((n, K), dtype=torch.float64, device=dev) for _ in range(2)]
-            step = lambda: M.spmv_complex_dev(dA, xs[0].data_ptr(), xs[1].data_ptr(), ys[0].data_ptr(),  # noqa
-                                              ys[1].data_ptr(), order, stream.cuda_stream)
+            if variant == "sptmv":
+                step = lambda: M.sptmv_complex_dev(dA, xs[0].data_ptr(), xs[1].data_ptr(), ys[0].data_ptr(),  # noqa
+                                                   ys[1].data_ptr(), order, False, stream.cuda_stream)
+            else:
+                step = lambda: M.spmv_complex_dev(dA, xs[0].data_ptr(), xs[1].data_ptr(), ys[0].data_ptr(),  # noqa
+                                                  ys[1].data_ptr(), order, stream.cuda_stream)
         else:
             dx = torch.from_numpy(x).to(dev)
             dy = torch.empty((n, K), dtype=torch.float64, device=dev)
-            step = lambda: M.spmv_dev(dA, dx.data_ptr(), dy.data_ptr(), order, stream.cuda_stream)  # noqa
+            if variant == "sptmv":
+                step = lambda: M.sptmv_dev(dA, dx.data_ptr(), dy.data_ptr(), order, stream.cuda_stream)  # noqa
+            else:
+                step = lambda: M.spmv_dev(dA, dx.data_ptr(), dy.data_ptr(), order, stream.cuda_stream)  # noqa
         for _ in range(args.warmup):
             step()
         ms = []
