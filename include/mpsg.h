@@ -201,7 +201,10 @@ MPSG_API int mpsg_csr_get_stats(const mpsg_csr* A, mpsg_csr_stats* out);
 /* Host pointers, synchronous: y[nrows*K] = A x[xlen*K]. */
 MPSG_API int mpsg_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen, const double* x,
               double* y);
-/* Device pointers, asynchronous on `stream` (NULL: the context stream). */
+/* Device pointers, asynchronous on `stream` (NULL: the context stream).
+ * DD / QD device vectors must be 16-byte aligned (every cudaMalloc pointer and
+ * every element offset into one is; TD: 8 bytes) -- MPSG_E_ARG otherwise.  A
+ * 32-byte aligned QD x is gathered with 256-bit loads. */
 MPSG_API int mpsg_spmv_dev(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* d_x, double* d_y,
                   void* stream);
 MPSG_API int mpsg_spmv_complex(mpsg_ctx* ctx, const mpsg_csr* A, int order, int64_t xlen,

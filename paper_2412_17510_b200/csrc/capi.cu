@@ -101,7 +101,7 @@ void free_csr(mpsg_csr* A) {
   void* ptrs[] = {A->slice_ptr, A->slot_row,    A->slot_len, A->scol,      A->sval,
                   A->lrow,      A->lptr,        A->lcol,     A->lval,      A->chunk_row,
                   A->chunk_beg, A->chunk_end,   A->chunk_slot, A->chunk_first, A->partial,
-                  A->counter};
+                  A->counter,   A->xpad};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete A;
@@ -136,10 +136,25 @@ int remap_rows(mpsg_ctx* ctx, mpsg_csr* A, const std::vector<int>& map) {
   return MPSG_OK;
 }
 
+// DD / QD device vectors are read and written with 128-bit (and, 32-byte
+// aligned, 256-bit) accesses: they must be 16-byte aligned (any cudaMalloc
+// pointer, and any element offset into one, is).  TD elements are 24 bytes and
+// take 64-bit accesses.
+static int check_vec_align(mpsg_ctx* ctx, const mpsg_csr* A, const double* xre, const double* xim,
+                           const double* yre, const double* yim) {
+  const uintptr_t m = (A->K == 3) ? 7 : 15;
+  const uintptr_t all = reinterpret_cast<uintptr_t>(xre) | reinterpret_cast<uintptr_t>(yre) |
+                        (A->cplx ? reinterpret_cast<uintptr_t>(xim) | reinterpret_cast<uintptr_t>(yim) : 0);
+  if (all & m)
+    return mpsg::fail(ctx, MPSG_E_ARG, "spmv: device vectors must be %d-byte aligned for K = %d", (int)m + 1, A->K);
+  return MPSG_OK;
+}
+
 int launch_spmv(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
                 double* yre, double* yim, cudaStream_t st, bool conj) {
   if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "spmv: unknown order %d", order);
   if (A->nrows == 0) return MPSG_OK;
+  if (int rc = check_vec_align(ctx, A, xre, xim, yre, yim)) return rc;
   if (!A->cplx) {
     switch (A->K) {
       case 2: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st, conj, -2);
@@ -160,6 +175,7 @@ int launch_spmv_part(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
                      double* yre, double* yim, cudaStream_t st, bool conj, int part) {
   if (order < 0 || order > 2) return fail(ctx, MPSG_E_ARG, "spmv: unknown order %d", order);
   if (A->nrows == 0) return MPSG_OK;
+  if (int rc = check_vec_align(ctx, A, xre, xim, yre, yim)) return rc;
   switch (A->K * 2 + (A->cplx ? 1 : 0)) {
     case 4: return launch_spmv_k<2, false>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
     case 5: return launch_spmv_k<2, true>(ctx, A, order, xre, xim, yre, yim, st, conj, part);
@@ -624,6 +640,13 @@ int mpsg_csr_upload_ex(mpsg_ctx* ctx, int K, int flags, int64_t nrows, int64_t n
         ncols, A->scol, A->sval, A->sell_elems, d_bad);
     CUDA_TRY(ctx, cudaGetLastError());
   }
+  // TD x padded to 32 bytes per element for the FAST short-row kernel (one
+  // 256-bit gather instead of three 64-bit ones: cfg2 TD 252 -> 224 us).  The
+  // re-layout costs a pass over x (56 bytes per column) per SpMV, so only
+  // matrices with enough gathers per column take it (cfg5, 7 per column:
+  // 106 -> 132 us with it).
+  if (K == 3 && !A->cplx && !A->mixed && (nnz - A->long_nnz) >= 12 * ncols && nnz >= (1 << 20))
+    if ((rc = dev_alloc(ctx, A, &A->xpad, (size_t)ncols * 4))) return rc;
   // long store
   if (A->nlong) {
     const int NS = A->cplx ? 4 : 1;

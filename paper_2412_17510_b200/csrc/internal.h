@@ -84,6 +84,10 @@ struct mpsg_csr {
   int* chunk_first = nullptr;
   double* partial = nullptr;
   unsigned* counter = nullptr;
+  // real TD only: x re-laid out to 32 bytes per element ([ncols][4], last
+  // double unused) before the FAST short-row kernel, so that every gather is
+  // one aligned 256-bit load = one L1 wavefront instead of three 64-bit ones
+  double* xpad = nullptr;
   int64_t device_bytes = 0;
   // host-call output parts: slices [part_slice[p], part_slice[p+1]) write rows
   // [part_row[p], part_row[p+1]) (besides long rows); empty = no overlap

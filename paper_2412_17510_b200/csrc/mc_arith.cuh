@@ -508,6 +508,121 @@ MPSG_DI MC<3> fma_acc(const MC<3>& acc, const MC<3>& a, const MC<3>& x) {
 #endif
 }
 #endif
+// Level accumulators (warp-specialised short-row kernel, spmv_ws.cuh): the
+// level sums (s0, u, v, w) of fma_acc kept UNNORMALISED across a short group
+// of products -- every two_sum error still drops one level, so the value is
+// the same exact sum up to the level-3 (level-2 for TD) roundings -- and swept
+// once per group (lvl_sweep: fma_acc's three backward quick-two-sums) instead
+// of once per product: QD 112 + 9/G, TD 45 + 6/G operations per nonzero
+// instead of 121 / 52, and the four level chains of consecutive products are
+// independent of each other (no serial dependence through the sweep).  The
+// group is kept short (G = 4) so a level sum never outgrows the level above
+// it by more than the few terms of one group.
+MPSG_DI void fma_lvl(MC<4>& r, const MC<4>& a, const MC<4>& x) {
+  double p, q, q0, q1, q2, e0, f1, f2, f3, f4, g;
+  double w = r.c[3];
+  two_prod(a.c[0], x.c[0], p, q0);  // level 0
+  two_sum(r.c[0], p, r.c[0], e0);
+  two_prod(a.c[0], x.c[1], p, q1);  // level 1: p1 p2 q0 e0
+  two_sum(r.c[1], p, r.c[1], f1);
+  two_prod(a.c[1], x.c[0], p, q2);
+  two_sum(r.c[1], p, r.c[1], f2);
+  two_sum(r.c[1], q0, r.c[1], f3);
+  two_sum(r.c[1], e0, r.c[1], f4);
+  two_prod(a.c[0], x.c[2], p, q);  // level 2: p3 p4 p5 q1 q2 f1..f4; errors and low parts to level 3
+  two_sum(r.c[2], p, r.c[2], g);
+  w = dadd(dadd(w, g), q);
+  two_prod(a.c[1], x.c[1], p, q);
+  two_sum(r.c[2], p, r.c[2], g);
+  w = dadd(dadd(w, g), q);
+  two_prod(a.c[2], x.c[0], p, q);
+  two_sum(r.c[2], p, r.c[2], g);
+  w = dadd(dadd(w, g), q);
+  two_sum(r.c[2], q1, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], q2, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], f1, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], f2, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], f3, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], f4, r.c[2], g);
+  w = dadd(w, g);
+  w = dfma(a.c[0], x.c[3], w);  // level 3
+  w = dfma(a.c[1], x.c[2], w);
+  w = dfma(a.c[2], x.c[1], w);
+  w = dfma(a.c[3], x.c[0], w);
+  r.c[3] = w;
+}
+MPSG_DI MC<4> lvl_sweep(const MC<4>& v) {
+  MC<4> r;
+  double h;
+  qts(v.c[2], v.c[3], h, r.c[3]);
+  qts(v.c[1], h, h, r.c[2]);
+  qts(v.c[0], h, r.c[0], r.c[1]);
+  return r;
+}
+MPSG_DI void fma_lvl(MC<3>& r, const MC<3>& a, const MC<3>& x) {
+  double p, q0, q1, q2, e0, f1, f2, f3, f4;
+  two_prod(a.c[0], x.c[0], p, q0);  // level 0
+  two_sum(r.c[0], p, r.c[0], e0);
+  two_prod(a.c[0], x.c[1], p, q1);  // level 1
+  two_sum(r.c[1], p, r.c[1], f1);
+  two_prod(a.c[1], x.c[0], p, q2);
+  two_sum(r.c[1], p, r.c[1], f2);
+  two_sum(r.c[1], q0, r.c[1], f3);
+  two_sum(r.c[1], e0, r.c[1], f4);
+  double w = dadd(dadd(dadd(dadd(dadd(dadd(r.c[2], f1), f2), f3), f4), q1), q2);  // level 2
+  w = dfma(a.c[0], x.c[2], w);
+  w = dfma(a.c[1], x.c[1], w);
+  w = dfma(a.c[2], x.c[0], w);
+  r.c[2] = w;
+}
+// Mixed mode (binary64 matrix value a): products x_i * a at level i.
+// QD 67 + 9/G, TD 33 + 6/G operations per nonzero.
+MPSG_DI void fma_lvl_d(MC<4>& r, const MC<4>& x, double a) {
+  double p, q0, q1, q2, e0, f1, f2, f3, g;
+  double w = r.c[3];
+  two_prod(x.c[0], a, p, q0);  // level 0
+  two_sum(r.c[0], p, r.c[0], e0);
+  two_prod(x.c[1], a, p, q1);  // level 1: p1 q0 e0
+  two_sum(r.c[1], p, r.c[1], f1);
+  two_sum(r.c[1], q0, r.c[1], f2);
+  two_sum(r.c[1], e0, r.c[1], f3);
+  two_prod(x.c[2], a, p, q2);  // level 2: p2 q1 f1..f3
+  two_sum(r.c[2], p, r.c[2], g);
+  w = dadd(dadd(w, g), q2);
+  two_sum(r.c[2], q1, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], f1, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], f2, r.c[2], g);
+  w = dadd(w, g);
+  two_sum(r.c[2], f3, r.c[2], g);
+  w = dadd(w, g);
+  r.c[3] = dfma(x.c[3], a, w);  // level 3
+}
+MPSG_DI void fma_lvl_d(MC<3>& r, const MC<3>& x, double a) {
+  double p, q0, q1, e0, f1, f2, f3;
+  two_prod(x.c[0], a, p, q0);  // level 0
+  two_sum(r.c[0], p, r.c[0], e0);
+  two_prod(x.c[1], a, p, q1);  // level 1
+  two_sum(r.c[1], p, r.c[1], f1);
+  two_sum(r.c[1], q0, r.c[1], f2);
+  two_sum(r.c[1], e0, r.c[1], f3);
+  const double w = dadd(dadd(dadd(dadd(r.c[2], f1), f2), f3), q1);  // level 2
+  r.c[2] = dfma(x.c[2], a, w);
+}
+MPSG_DI MC<2> lvl_sweep(const MC<2>& v) { return v; }
+MPSG_DI MC<3> lvl_sweep(const MC<3>& v) {
+  MC<3> r;
+  double h;
+  qts(v.c[1], v.c[2], h, r.c[2]);
+  qts(v.c[0], h, r.c[0], r.c[1]);
+  return r;
+}
 // DD: the product's (p1, p2) without its quick_two_sum, straight into the add
 MPSG_DI MC<2> fma_fast(const MC<2>& acc, const MC<2>& a, const MC<2>& x) {
   double p1, p2;
@@ -746,9 +861,14 @@ MPSG_DI void ld_v4(const double* q, double& a, double& b, double& c, double& d) 
 // 64-bit loads (cfg2 TD 126.0 -> 123.0 Gnnz/s) and was dropped.
 template <int K>
 MPSG_DI MC<K> load_x_wide(const double* __restrict__ p, int64_t i) {
-  static_assert(K == 4, "256-bit gathers are used for QD only");
+  static_assert(K == 4 || K == 3, "256-bit gathers: QD, and TD from the padded copy of x ([n][4])");
   MC<K> r;
-  ld_v4(p + 4 * i, r.c[0], r.c[1], r.c[2], r.c[3]);
+  if constexpr (K == 4) {
+    ld_v4(p + 4 * i, r.c[0], r.c[1], r.c[2], r.c[3]);
+  } else {
+    double pad;
+    ld_v4(p + 4 * i, r.c[0], r.c[1], r.c[2], pad);
+  }
   return r;
 }
 

@@ -62,6 +62,13 @@ struct AVal<K, false> {  // Pure: K component planes, mul(a, v)
   MPSG_DI MC<K> times(const MC<K>& v) const { return mul(a, v); }
   // FAST order: acc + a*v with one renormalisation (mc_arith.cuh fma_fast)
   MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_acc(acc, a, v); }
+  // TD/QD: into unnormalised level sums (fma_lvl, swept per group by the caller)
+  MPSG_DI void accumulate_lvl(MC<K>& acc, const MC<K>& v) const {
+    if constexpr (K >= 3)
+      fma_lvl(acc, a, v);
+    else
+      acc = fma_acc(acc, a, v);
+  }
 };
 template <int K>
 struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
@@ -71,6 +78,12 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
   MPSG_DI void load_ldg(const double* __restrict__ vp, int64_t, int64_t e) { a = __ldg(vp + e); }
   MPSG_DI MC<K> times(const MC<K>& v) const { return mul_d(v, a); }
   MPSG_DI MC<K> accumulate(const MC<K>& acc, const MC<K>& v) const { return fma_acc_d(acc, v, a); }
+  MPSG_DI void accumulate_lvl(MC<K>& acc, const MC<K>& v) const {
+    if constexpr (K >= 3)
+      fma_lvl_d(acc, v, a);
+    else
+      acc = fma_acc_d(acc, v, a);
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -99,16 +112,36 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 #ifndef MPSG_FUSED_G_QD
 #define MPSG_FUSED_G_QD 4
 #endif
+#ifndef MPSG_FUSED_G_TD
+#define MPSG_FUSED_G_TD 2
+#endif
+// FAST short rows: the products of a round go into unnormalised level sums
+// (fma_lvl) and the backward sweep runs once per round instead of once per
+// product (mc_arith.cuh).
+#ifndef MPSG_LVL_ACC
+#define MPSG_LVL_ACC 1
+#endif
 
 // x gather in the real SELL kernels: QD with one 256-bit load when x is
 // 32-byte aligned (the kernel's XW flag, checked per launch), else the plain
 // AoS loads.
 template <int K>
 MPSG_DI MC<K> load_x(const double* __restrict__ x, bool xw, int64_t i) {
-  if constexpr (K == 4) {
-    if (xw) return load_x_wide<K>(x, i);
+  if constexpr (K == 4 || K == 3) {
+    if (xw) return load_x_wide<K>(x, i);  // TD: x is the padded copy
   }
   return load_aos<K>(x, i);
+}
+
+// TD x [n][3] -> [n][4] (see mpsg_csr::xpad): four consecutive elements are
+// three 256-bit loads and four 256-bit stores per thread.
+static __global__ void __launch_bounds__(256) pad_td_kernel(const double* __restrict__ x, double* __restrict__ xp, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = __ldg(x + 3 * i), b = __ldg(x + 3 * i + 1), c = __ldg(x + 3 * i + 2);
+  double4 v = make_double4(a, b, c, 0.0);
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(xp + 4 * i), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+               : "memory");
 }
 
 // Product term of slot-row element k.
@@ -172,7 +205,7 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
 template <int K, bool MX, bool FUSED = false>
 MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ cp, int64_t st,
                          const double* __restrict__ x, bool xw, int len) {
-  constexpr int G = K == 2 ? 4 : (FUSED ? (K == 4 ? MPSG_FUSED_G_QD : 2) : 2);
+  constexpr int G = K == 2 ? 4 : (FUSED ? (K == 4 ? MPSG_FUSED_G_QD : MPSG_FUSED_G_TD) : 2);
   constexpr bool PF = K != 2;
   MC<K> acc = zero<K>();
   int k = 0;
@@ -192,8 +225,14 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
           a[j].load(vp, st, (int64_t)(k + j) * 32);
           v[j] = load_x<K>(x, xw, c[j]);
         }
+#if MPSG_LVL_ACC
+#pragma unroll
+        for (int j = 0; j < G; ++j) a[j].accumulate_lvl(acc, v[j]);
+        acc = lvl_sweep(acc);
+#else
 #pragma unroll
         for (int j = 0; j < G; ++j) acc = a[j].accumulate(acc, v[j]);
+#endif
       } else {
         MC<K> p[G];
 #pragma unroll
@@ -215,11 +254,19 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
       if (k + j < len) {
         AVal<K, MX> a;
         a.load(vp, st, (int64_t)(k + j) * 32);
-        if constexpr (FUSED)
+        if constexpr (FUSED) {
+#if MPSG_LVL_ACC
+          a.accumulate_lvl(acc, load_x<K>(x, xw, c[j]));
+#else
           acc = a.accumulate(acc, load_x<K>(x, xw, c[j]));
-        else
+#endif
+        } else {
           acc = add(acc, a.times(load_x<K>(x, xw, c[j])));
+        }
       }
+#if MPSG_LVL_ACC
+    if constexpr (FUSED) acc = lvl_sweep(acc);
+#endif
     if constexpr (FUSED) acc = canon(acc);
     return acc;
   } else {

@@ -265,7 +265,9 @@ def test_host_call_overlapped_parts(K, order):
 @pytest.mark.parametrize("order", [0, 1, 2])
 def test_unaligned_device_x_takes_the_narrow_gather(order):
     """QD x gathers use 256-bit loads only when x is 32-byte aligned; an x
-    that starts 8 bytes into an allocation must give the same result."""
+    that starts 16 bytes into an allocation (the ABI's minimum alignment for
+    DD / QD device vectors) must give the same result, and an 8-byte offset is
+    refused (MPSG_E_ARG) instead of faulting."""
     import torch
 
     c = M.Context(0)
@@ -273,14 +275,17 @@ def test_unaligned_device_x_takes_the_narrow_gather(order):
     A = synth.config_matrix(2, K, 3000)
     x = synth.config_vector(2, A.nrows, K)
     dA = M.DeviceCsr(A, K, ctx=c)
-    flat = torch.zeros(A.nrows * K + 1, dtype=torch.float64, device="cuda")
-    flat[1:] = torch.from_numpy(x.reshape(-1)).cuda()
-    assert (flat.data_ptr() + 8) % 32 != 0
+    flat = torch.zeros(A.nrows * K + 2, dtype=torch.float64, device="cuda")
+    flat[2:] = torch.from_numpy(x.reshape(-1)).cuda()
+    assert (flat.data_ptr() + 16) % 32 != 0
     dy = torch.empty((A.nrows, K), dtype=torch.float64, device="cuda")
-    M.spmv_dev(dA, flat.data_ptr() + 8, dy.data_ptr(), order, None)
+    M.spmv_dev(dA, flat.data_ptr() + 16, dy.data_ptr(), order, None)
     c.synchronize()
     aligned = M.spmv(dA, x, order)
     assert bits_equal(dy.cpu().numpy(), aligned)
     if order != 2:
         assert bits_equal(aligned, O.spmv(A, x, order))
+    with pytest.raises(M.MpsgError) as ei:
+        M.spmv_dev(dA, flat.data_ptr() + 8, dy.data_ptr(), order, None)
+    assert ei.value.code == 6 and "aligned" in str(ei.value)
     c.close()
