@@ -64,7 +64,13 @@ OPS_PER_NNZ_MIXED = {2: 17, 3: 130, 4: 152}
 OPS_FAST = {2: 17, 3: 52, 4: 121}
 OPS_FAST_MIXED = {2: 17, 3: 114, 4: 76}
 OPS_FAST_UPDATE = {2: 20, 3: 68, 4: 143}
-ROW_CANON = {2: 0, 3: 16, 4: 22}
+# Real short rows (sell_real_kernel, FAST): the products of a round of G go
+# into unnormalised level sums (fma_lvl: QD 12 + 84 + 16 = 112, TD 6 + 30 + 9 =
+# 45; Mixed QD 67, TD 33) and the backward sweep (QD 9, TD 6) runs once per
+# round (G = 4 QD, 2 TD), once more at the row's end, then the row's renorm.
+OPS_FAST_SELL = {2: 17, 3: 45 + 6 / 2, 4: 112 + 9 / 4}
+OPS_FAST_SELL_MIXED = {2: 17, 3: 33 + 6 / 2, 4: 67 + 9 / 4}
+ROW_CANON = {2: 0, 3: 16 + 6, 4: 22 + 9}
 K_NAME = {2: "DD", 3: "TD", 4: "QD"}
 ORDER_NAME = {0: "scalar", 1: "lane4", 2: "fast"}
 CG_ITERS = 500
@@ -78,9 +84,11 @@ def algorithmic_bytes(nnz, n, K, cplx, mixed=False):
 
 
 def algorithmic_ops(nnz, K, cplx, mixed=False, n=0, fast=False):
+    if fast and cplx:  # four real sums per nonzero; Pure keeps the sweep per product (fma_acc)
+        return nnz * 4 * (OPS_FAST_SELL_MIXED if mixed else OPS_FAST)[K]
     if fast:
-        per = (OPS_FAST_MIXED if mixed else OPS_FAST)[K]
-        return nnz * per * (4 if cplx else 1) + (0 if cplx else n * ROW_CANON[K])
+        per = (OPS_FAST_SELL_MIXED if mixed else OPS_FAST_SELL)[K]
+        return nnz * per + n * ROW_CANON[K]
     return nnz * (OPS_PER_NNZ_MIXED if mixed else OPS_PER_NNZ)[K] * (4 if cplx else 1)
 
 
@@ -92,7 +100,7 @@ def cg_iter_bytes(nnz, n, K):
 def cg_iter_ops(nnz, n, K, fast=False):
     if fast:  # SpMV + <p,q>, <r,r> accumulations + x, r, p stored updates (cg_kernels.cuh)
         vec = 2 * OPS_FAST[K] + 3 * OPS_FAST_UPDATE[K] if K > 2 else 5 * OPS_PER_NNZ[K]
-        return nnz * OPS_FAST[K] + n * ROW_CANON[K] + n * vec
+        return nnz * OPS_FAST_SELL[K] + n * ROW_CANON[K] + n * vec
     return (nnz + 5 * n) * OPS_PER_NNZ[K]
 
 
@@ -114,7 +122,7 @@ def solver_iter_ops(method, nnz, n, K, fast=False):
     s, pairs, _ = SOLVER_WORK[method]
     if fast:  # BiCGSTAB: 6 dot accumulations, 5 fused stored updates, 1 plain (p - omega v)
         vec = 6 * OPS_FAST[K] + 5 * OPS_FAST_UPDATE[K] + OPS_PER_NNZ[K] if K > 2 else pairs * OPS_PER_NNZ[K]
-        return s * (nnz * OPS_FAST[K] + n * ROW_CANON[K]) + n * vec
+        return s * (nnz * OPS_FAST_SELL[K] + n * ROW_CANON[K]) + n * vec
     return (s * nnz + pairs * n) * OPS_PER_NNZ[K]
 
 

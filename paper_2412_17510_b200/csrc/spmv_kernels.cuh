@@ -99,8 +99,15 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 // minBlocks 0 compiles to the same SASS as no bound (40 registers, 32 in Mixed
 // mode); a 64 cap let it grow (cfg5 DD 228 -> 197 Gnnz/s) and a 12-block cap
 // changed its schedule (-6%).
+// TD with the level accumulators: 7 resident blocks (72 registers, no spills)
+// beat 8 (cfg2 TD 222 -> 196 us, cfg5 TD 103 -> 97 us); QD keeps 8 (72
+// registers: cfg2 QD 292 -> 325 us).
+#ifndef MPSG_SELL_MINB_TD
+#define MPSG_SELL_MINB_TD 7
+#endif
 #if MPSG_SELL_MINB > 0
-#define MPSG_SELL_LB __launch_bounds__(128, (K == 2 ? 0 : MPSG_SELL_MINB))
+#define MPSG_SELL_LB \
+  __launch_bounds__(128, (K == 2 ? 0 : (K == 3 && ORDER == ORDER_FAST ? MPSG_SELL_MINB_TD : MPSG_SELL_MINB)))
 #else
 #define MPSG_SELL_LB __launch_bounds__(128)
 #endif
@@ -443,9 +450,18 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
       const int cn = (k + 1 < len) ? ld_s32_stream(cp + e + 16) : 0;
       AVal<K, MX> a;
       a.load(vp, st, e);
-      if constexpr (ORDER == ORDER_FAST) {  // one renormalisation per product-accumulate
+      if constexpr (ORDER == ORDER_FAST && !MX) {  // one renormalisation sweep per product-accumulate
+        // (Pure mode: the level sums with a sweep per four products measured
+        // slower here, cfg3 QD 29.6 -> 26.5 Gnnz/s: two accumulators per thread)
         s1 = a.accumulate(s1, load_aos<K>(x1, c));
         s2 = a.accumulate(s2, load_aos<K>(x2, c));
+      } else if constexpr (ORDER == ORDER_FAST) {  // Mixed: level sums, one backward sweep per four products
+        a.accumulate_lvl(s1, load_aos<K>(x1, c));
+        a.accumulate_lvl(s2, load_aos<K>(x2, c));
+        if ((k & 3) == 3 || k + 1 == len) {
+          s1 = lvl_sweep(s1);
+          s2 = lvl_sweep(s2);
+        }
       } else {
         MC<K> p1 = a.times(load_aos<K>(x1, c));
         MC<K> p2 = a.times(load_aos<K>(x2, c));
@@ -614,20 +630,32 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
       MC<K> v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = load_aos<K>(xre, c[u]);
+      if constexpr (K >= 3) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[0] = fma_acc_d(acc[0], v[u], a[u]);
+        for (int u = 0; u < U; ++u) fma_lvl_d(acc[0], v[u], a[u]);
+        acc[0] = lvl_sweep(acc[0]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[0] = fma_acc_d(acc[0], v[u], a[u]);
+      }
     }
-    for (; k < e; k += 32)
-      acc[0] = fma_acc_d(acc[0], load_aos<K>(xre, ld_s32_stream(L.col + k)), ld_f64_stream(L.val + k));
+    for (; k < e; k += 32) {
+      AVal<K, MX> a1;
+      a1.load(L.val, L.stride, k);
+      a1.accumulate_lvl(acc[0], load_aos<K>(xre, ld_s32_stream(L.col + k)));
+      acc[0] = lvl_sweep(acc[0]);
+    }
   } else if constexpr (!CPLX) {
     int c = k < e ? ld_s32_stream(L.col + k) : 0;
-    for (; k < e; k += 32) {
+    for (int it = 0; k < e; k += 32, ++it) {
       const int cn = k + 32 < e ? ld_s32_stream(L.col + k + 32) : 0;
       AVal<K, MX> a;
       a.load(L.val, L.stride, k);
-      acc[0] = a.accumulate(acc[0], load_aos<K>(xre, c));  // FAST: one renormalisation per nonzero
+      a.accumulate_lvl(acc[0], load_aos<K>(xre, c));  // FAST: level sums, swept every four products
+      if ((it & 3) == 3) acc[0] = lvl_sweep(acc[0]);
       c = cn;
     }
+    acc[0] = lvl_sweep(acc[0]);
   } else {
     for (; k < e; k += 32) {
       const int c = ld_s32_stream(L.col + k);
@@ -635,10 +663,12 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
       are.load(L.val, L.stride, k);
       aim.load(L.val + (int64_t)AVal<K, MX>::NPL * L.stride, L.stride, k);
       MC<K> vr = load_aos<K>(xre, c), vi = load_aos<K>(xim, c);
-      acc[0] = are.accumulate(acc[0], vr);
-      acc[1] = aim.accumulate(acc[1], vi);
-      acc[2] = are.accumulate(acc[2], vi);
-      acc[3] = aim.accumulate(acc[3], vr);
+      are.accumulate_lvl(acc[0], vr);
+      aim.accumulate_lvl(acc[1], vi);
+      are.accumulate_lvl(acc[2], vi);
+      aim.accumulate_lvl(acc[3], vr);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) acc[s] = lvl_sweep(acc[s]);
     }
   }
 #pragma unroll
