@@ -2,7 +2,6 @@
 #pragma once
 #include "internal.h"
 #include "spmv_kernels.cuh"
-#include "spmv_ws.cuh"
 
 #include <cstdlib>
 
@@ -17,24 +16,6 @@ namespace mpsg {
 // concurrently with the SELL kernel on `st`.  part = -2: all of it;
 // part = -1: only the long-row kernel, on `st`; part >= 0: only the SELL
 // slices of output part `part` (host-call overlap, capi.cu).
-// Warp-specialised FAST short-row kernel (spmv_ws.cuh): TD/QD, Pure mode.
-// MPSG_WS=0 in the environment falls back to the plain FAST kernel.
-#ifndef MPSG_WS_NC
-#define MPSG_WS_NC 4
-#endif
-#ifndef MPSG_WS_S
-#define MPSG_WS_S 4
-#endif
-#ifndef MPSG_WS_NPW
-#define MPSG_WS_NPW 2
-#endif
-inline bool ws_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("MPSG_WS");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
 inline bool td_pad_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("MPSG_TD_PAD");
@@ -42,25 +23,6 @@ inline bool td_pad_enabled() {
   }();
   return on;
 }
-template <int K, bool MX, bool XPAD>
-int launch_sell_ws(mpsg_ctx* ctx, const SellView& S, const double* x, double* y, cudaStream_t st) {
-  constexpr int NC = MPSG_WS_NC, SG = MPSG_WS_S;
-  constexpr int smem = ws::ws_smem_bytes<K, MX, NC, SG>();
-  auto kern = ws::sell_ws_kernel<K, MX, NC, SG, MPSG_WS_NPW, XPAD>;
-  static bool configured[16] = {};
-  const int dev = ctx->device & 15;
-  if (!configured[dev]) {
-    CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                       cudaSharedmemCarveoutMaxShared));
-    configured[dev] = true;
-  }
-  const int blocks = (S.nslices + NC - 1) / NC;
-  kern<<<blocks, (NC + MPSG_WS_NPW) * 32, smem, st>>>(S, x, y);
-  CUDA_TRY(ctx, cudaGetLastError());
-  return MPSG_OK;
-}
-
 template <int K, bool CPLX, bool MX, bool CONJ>
 int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* xre, const double* xim,
                      double* yre, double* yim, cudaStream_t st, int part) {
@@ -98,9 +60,10 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
   }
   const SellView S = part >= 0 ? A->sell_range(A->part_slice[(size_t)part], A->part_slice[(size_t)part + 1])
                                : A->sell();
-  // 256-bit x gathers (QD real kernels) need a 32-byte aligned x.  TD keeps
-  // its three 64-bit loads: the windowed 256-bit TD gather (load_x_wide<3>)
-  // measured slower (cfg2 TD 126.0 -> 123.0, cfg5 TD 134.3 -> 121.7 Gnnz/s).
+  // 256-bit x gathers (QD real kernels) need a 32-byte aligned x.  TD takes
+  // them from the padded copy of x (mpsg_csr::xpad, FAST order, matrices with
+  // enough gathers per column); a windowed 256-bit gather on the unpadded
+  // [n][3] vector measured slower than three 64-bit loads.
   const bool xw = K == 4 && (reinterpret_cast<uintptr_t>(xre) & 31) == 0;
   if (part != -1 && S.nslices > 0) {
     const int blocks = (S.nslices + 3) / 4;
@@ -116,19 +79,7 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
     if constexpr (!CPLX) {
       if (seg)
         sell_real_seg_kernel<K, MX><<<blocks, 128, 0, st>>>(S, xre, yre, ctx->seg_bounds, ctx->seg_T);
-      else if (order == ORDER_FAST && MPSG_FUSED && K >= 3 && !MX && ws_enabled() &&
-               (reinterpret_cast<uintptr_t>(xre) & (K == 4 ? 31 : 7)) == 0) {
-        if constexpr (K >= 3 && !MX) {
-          int rc;
-          if (K == 3 && A->xpad && td_pad_enabled()) {
-            pad_td_kernel<<<(unsigned)((A->ncols + 255) / 256), 256, 0, st>>>(xre, A->xpad, A->ncols);
-            rc = launch_sell_ws<K, MX, true>(ctx, S, A->xpad, yre, st);
-          } else {
-            rc = launch_sell_ws<K, MX, K == 4>(ctx, S, xre, yre, st);
-          }
-          if (rc != MPSG_OK) return rc;
-        }
-      } else if (order == ORDER_FAST && MPSG_FUSED && K == 3 && A->xpad && td_pad_enabled()) {
+      else if (order == ORDER_FAST && MPSG_FUSED && K == 3 && A->xpad && td_pad_enabled()) {
         if constexpr (K == 3) {
           pad_td_kernel<<<(unsigned)((A->ncols + 255) / 256), 256, 0, st>>>(xre, A->xpad, A->ncols);
           CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_FAST, MX, true>, blocks, 128, 0, st, xre, xb, S,
