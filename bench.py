@@ -525,7 +525,8 @@ def run_gpu_cg(args, K, order, rank, world, dist, method="cg"):
     shard = args.shard and world > 1 and method == "cg"
     iters = CG_ITERS if method == "cg" else SOLVER_ITERS
     cfg = M.SolverConfig(method=M.parse_method(method), rel_tol=1e-30 if method == "cg" else 1e-99,
-                         max_iters=iters, lanes_enabled=order != 0, fast=order == 2)
+                         max_iters=iters, lanes_enabled=order != 0, fast=order == 2,
+                         cg_variant=getattr(args, "cg_variant", 0))
     comm = None
     if method != "cg":
         dA = M.DeviceCsr(A, K, ctx=ctx)
@@ -625,6 +626,8 @@ def main():
     ap.add_argument("--order", default="fast", choices=["fast", "lane4", "scalar"])
     ap.add_argument("--shard", action="store_true", help="row-shard the matrix across ranks (configs 3, 4, 5)")
     ap.add_argument("--cg", action="store_true", help="config 5: 500-iteration CG instead of one SpMV")
+    ap.add_argument("--cg-variant", type=int, default=0, choices=[0, 1, 2],
+                    help="--cg: 0 auto (classic on one GPU, one reduction per iteration when sharded), 1 classic, 2 one reduction")
     ap.add_argument("--solver", default="", help="config 5: a device solver (bicgstab) instead of one SpMV")
     ap.add_argument("--variant", default="pure", choices=["pure", "mixed", "sptmv"],
                     help="mixed: binary64 matrix (the paper's M mode); sptmv: y = A^T x")
@@ -752,6 +755,10 @@ def main():
                                            "batches of 32)",
                                       iterations=r["iterations"], rel_residual=r["rel_residual"],
                                       true_residual=r["true_residual"])
+                if r["method"] == "cg":
+                    one = args.cg_variant == 2 or (args.cg_variant == 0 and r["shard"])
+                    line["config"]["cg_form"] = ("one reduction per iteration (Chronopoulos-Gear)" if one else
+                                                 "reference form, two reductions per iteration")
                 line["ms_per_iteration"] = r["per_iter"] * 1e3
             if r["shard"]:
                 line["config"]["halo_rows_rank0"] = r["halo_rows"]

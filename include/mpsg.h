@@ -136,7 +136,16 @@ typedef struct mpsg_cg_config {
   int64_t max_iters;  /* default 10000 */
   int32_t check_every; /* host polls the device status every N iterations (0 = 32) */
   int32_t use_graph;   /* capture the iteration batch in a CUDA graph (default 1) */
+  int32_t variant;     /* mpsg_cg_variant (0 = auto) */
+  int32_t reserved;
 } mpsg_cg_config;
+
+/* CG iteration form.  CLASSIC is the reference's (krylov.hpp:238-281: two dot
+ * products per iteration); ONE_REDUCTION is the Chronopoulos-Gear recurrence
+ * with the same Krylov iterates and a single fused reduction (<r,r>, <Ar,r>)
+ * per iteration -- one allgather per iteration when the rows are sharded.
+ * AUTO: CLASSIC on one GPU, ONE_REDUCTION for mpsg_dcg over more than one rank. */
+typedef enum mpsg_cg_variant { MPSG_CG_AUTO = 0, MPSG_CG_CLASSIC = 1, MPSG_CG_ONE_REDUCTION = 2 } mpsg_cg_variant;
 
 /* SolverConfig (krylov.hpp:58-75) for mpsg_solve. */
 typedef struct mpsg_solver_config {

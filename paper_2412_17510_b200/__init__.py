@@ -64,7 +64,8 @@ class CsrStats(ctypes.Structure):
 
 class _CgConfig(ctypes.Structure):
     _fields_ = [("rel_tol", _f64), ("abs_tol", _f64), ("max_iters", _i64),
-                ("check_every", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+                ("check_every", ctypes.c_int32), ("use_graph", ctypes.c_int32),
+                ("variant", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class _SolverConfig(ctypes.Structure):
@@ -412,6 +413,10 @@ class SolverConfig:  # krylov.hpp:58-75
     # reference dot order (one device thread per dot, krylov.hpp:122-128): with
     # an exact SpMV order the device solve reproduces the reference's bits
     exact_dots: bool = False
+    # CG iteration form (mpsg_cg_variant): 0 auto (the reference's two-reduction
+    # iteration on one GPU, the one-reduction Chronopoulos-Gear form when sharded
+    # over several ranks), 1 classic, 2 one reduction per iteration
+    cg_variant: int = 0
 
     def validate(self):
         if not (self.rel_tol > 0.0) or not (self.abs_tol > 0.0):
@@ -420,6 +425,8 @@ class SolverConfig:  # krylov.hpp:58-75
             raise ValueError("solver: max_iters must be at least 1")
         if self.threads < 1:
             raise ValueError("solver: threads must be at least 1")
+        if self.cg_variant not in (0, 1, 2):
+            raise ValueError("solver: cg_variant must be 0 (auto), 1 (classic) or 2 (one reduction)")
 
 
 @dataclass
@@ -484,7 +491,8 @@ def solve_cg(op: CsrOperator, b, cfg: SolverConfig | None = None) -> SolveResult
             raise ValueError("solver: x0 length does not match the rhs")
         x0 = np.zeros_like(bb)
         x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)  # scalar_like (krylov.hpp:178)
-    c = _CgConfig(cfg.rel_tol, cfg.abs_tol, cfg.max_iters, cfg.check_every, 1 if cfg.use_graph else 0)
+    c = _CgConfig(cfg.rel_tol, cfg.abs_tol, cfg.max_iters, cfg.check_every, 1 if cfg.use_graph else 0,
+                  int(cfg.cg_variant), 0)
     rep = _CgReport()
     x = np.empty_like(bb)
     hist = np.empty(cfg.max_iters + 1)
@@ -707,7 +715,8 @@ def dsolve_cg(A: DistCsr, b_local, cfg: SolverConfig | None = None) -> SolveResu
             raise ValueError("solver: x0 length does not match the rhs")
         x0 = np.zeros_like(bb)
         x0[:, 0] = np.asarray(cfg.x0, dtype=np.float64)[A.row_begin:A.row_end]
-    c = _CgConfig(cfg.rel_tol, cfg.abs_tol, cfg.max_iters, cfg.check_every, 1 if cfg.use_graph else 0)
+    c = _CgConfig(cfg.rel_tol, cfg.abs_tol, cfg.max_iters, cfg.check_every, 1 if cfg.use_graph else 0,
+                  int(cfg.cg_variant), 0)
     rep = _CgReport()
     x = np.empty_like(bb)
     hist = np.empty(cfg.max_iters + 1)

@@ -272,22 +272,4 @@ int cg_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, int order, c
 #undef CG_RC
 }
 
-template <int K>
-int run_cg(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* b_host, const double* x0,
-           const mpsg_cg_config* cfg, double* x_out, double* history, int64_t history_cap, mpsg_cg_report* rep) {
-  return cg_driver<K>(ctx, A, nullptr, order, b_host, x0, cfg, x_out, history, history_cap, rep);
-}
-
-template <int K>
-int run_dcg(mpsg_dcsr* D, int order, const double* b_host, const double* x0, const mpsg_cg_config* cfg,
-            double* x_out, double* history, int64_t history_cap, mpsg_cg_report* rep) {
-  return cg_driver<K>(D->comm->ctx, D->local, D, order, b_host, x0, cfg, x_out, history, history_cap, rep);
-}
-
 }  // namespace mpsg
-
-#define MPSG_INSTANTIATE_CG(K)                                                                            \
-  template int mpsg::run_cg<K>(mpsg_ctx*, const mpsg_csr*, int, const double*, const double*,              \
-                               const mpsg_cg_config*, double*, double*, int64_t, mpsg_cg_report*);         \
-  template int mpsg::run_dcg<K>(mpsg_dcsr*, int, const double*, const double*, const mpsg_cg_config*,      \
-                                double*, double*, int64_t, mpsg_cg_report*);

@@ -1,3 +1,3 @@
 // Device CG for K = 3.
-#include "cg_inst.cuh"
+#include "cg1r_inst.cuh"
 MPSG_INSTANTIATE_CG(3)

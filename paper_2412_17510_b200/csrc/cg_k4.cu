@@ -1,3 +1,3 @@
 // Device CG for K = 4.
-#include "cg_inst.cuh"
+#include "cg1r_inst.cuh"
 MPSG_INSTANTIATE_CG(4)

@@ -108,9 +108,78 @@ def test_cg_config_errors(ctx):
         M.solve_cg(M.CsrOperator(M.DeviceCsr(R, 2, ctx=ctx)), b)
 
 
+# ---- one reduction per iteration (Chronopoulos-Gear form, mpsg_cg_variant 2) ----------
+@pytest.mark.parametrize("K", [2, 3, 4])
+@pytest.mark.parametrize("graph", [True, False])
+def test_cg_one_reduction_small_tracks_reference(ctx, K, graph):
+    """The single-reduction recurrence builds the same Krylov iterates: its
+    residual history tracks the reference's (krylov.hpp:238-281) until round-off
+    dominates, with the reference's report semantics (odd check_every: both
+    state parities are polled)."""
+    g = golden("cg_small")
+    A = synth.config_matrix(5, K, p1=10)
+    xt = synth.config_vector(5, A.nrows, K)
+    b = O.spmv(A, xt, 1)
+    dA = M.DeviceCsr(A, K, ctx=ctx)
+    res = M.solve_cg(M.CsrOperator(dA), b, M.SolverConfig(rel_tol=1e-30, max_iters=80, use_graph=graph,
+                                                          check_every=7, cg_variant=2))
+    ref_h = g[f"cg5s_K{K}_history"]
+    meta = g[f"cg5s_K{K}_meta"]
+    rep = res.report
+    assert rep.status == M.SolverStatus.MaxIterations and rep.iterations == 80 == meta[0]
+    assert len(rep.residual_history) == 81
+    h = np.asarray(rep.residual_history)
+    assert abs(h[0] - ref_h[0]) <= 1e-14 * ref_h[0] and rep.rhs_norm == meta[2]
+    rel = np.abs(h - ref_h) / ref_h
+    assert np.all(rel[:60] < 1e-6), rel[:60].max()
+    assert rep.final_true_residual < 1e-6
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_cg_one_reduction_converges_like_reference(ctx, K):
+    g = golden("cg_small")
+    A = synth.config_matrix(5, K, p1=10)
+    xt = synth.config_vector(5, A.nrows, K)
+    b = O.spmv(A, xt, 1)
+    res = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, K, ctx=ctx)), b,
+                     M.SolverConfig(rel_tol=1e-20, max_iters=400, cg_variant=2))
+    meta = g[f"cg5c_K{K}_meta"]
+    assert res.report.status == M.SolverStatus.Converged and res.report.converged
+    assert abs(res.report.iterations - meta[0]) <= max(1, int(0.01 * meta[0]))
+    assert len(res.report.residual_history) == res.report.iterations + 1
+    assert np.allclose(res.x[:, 0], xt[:, 0], atol=1e-12)
+
+
+def test_cg_one_reduction_report_semantics(ctx):
+    """Breakdown at the first <p, Ap>, exact initial guess, x0 start, diagonal
+    system: the reference's statuses, counts and texts (test_krylov.cpp:94-116,
+    193-211, 231-251)."""
+    A = csr(2, 2, [[1], [0]], 2, planes=np.array([[1.0, -1.0], [0.0, 0.0]]))
+    r = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, 2, ctx=ctx)), np.array([[1.0, 0.0], [1.0, 0.0]]),
+                   M.SolverConfig(cg_variant=2)).report
+    assert r.status == M.SolverStatus.Breakdown and not r.converged and r.iterations == 0
+    assert len(r.residual_history) == 1 and r.detail == "cg: <p, Ap> vanished"
+    assert abs(r.final_true_residual - np.sqrt(2.0)) < 1e-15
+    A = csr(3, 3, [[0], [1], [2]], 2, planes=np.array([[1.0, 2.0, 4.0], [0.0, 0.0, 0.0]]))
+    b = np.array([[1.0, 0.0], [4.0, 0.0], [16.0, 0.0]])
+    res = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, 2, ctx=ctx)), b, M.SolverConfig(x0=[1.0, 2.0, 4.0], cg_variant=2))
+    assert res.report.converged and res.report.iterations == 0
+    assert res.report.residual_history == [0.0] and res.x[1, 0] == 2.0
+    res = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, 2, ctx=ctx)), b, M.SolverConfig(x0=[0.5, 0.5, 0.5], cg_variant=2))
+    assert res.report.converged and res.report.iterations <= 4
+    assert np.allclose(res.x[:, 0], [1.0, 2.0, 4.0], atol=1e-13)
+    g = golden("cg_small")
+    k = 40
+    D = csr(k, k, [[i] for i in range(k)], 4, planes=np.vstack([np.arange(1, k + 1, dtype=float), np.zeros((3, k))]))
+    res = M.solve_cg(M.CsrOperator(M.DeviceCsr(D, 4, ctx=ctx)), g["diag40_b"],
+                     M.SolverConfig(rel_tol=1e-50, cg_variant=2))
+    assert res.report.converged and abs(res.report.iterations - int(g["diag40_meta"][0])) <= 1
+
+
+@pytest.mark.parametrize("variant", [1, 2], ids=["classic", "one_reduction"])
 @pytest.mark.parametrize("fast", [False, True], ids=["lane4", "fast"])
 @pytest.mark.parametrize("K", [2, 4])
-def test_cg_full_config5_500_iterations(ctx, K, fast):
+def test_cg_full_config5_500_iterations(ctx, K, fast, variant):
     """Config 5 (3D 7-pt Laplacian 128^3 + 1e-3 shift), 500 iterations: the GPU
     reaches the reference's final residual within 500 +- 5 iterations -- in the
     bit-exact LANE4 order and in the FAST order bench.py times (fused
@@ -125,7 +194,8 @@ def test_cg_full_config5_500_iterations(ctx, K, fast):
     b = M.spmv(dA, xt, M.ORDER_LANE4)
     assert M.checksum(b) == int(g[f"cg5_K{K}_b_checksum"])
     ref_h = g[f"cg5_K{K}_history"]
-    res = M.solve_cg(M.CsrOperator(dA), b, M.SolverConfig(rel_tol=1e-30, max_iters=510, fast=fast))
+    res = M.solve_cg(M.CsrOperator(dA), b, M.SolverConfig(rel_tol=1e-30, max_iters=510, fast=fast,
+                                                          cg_variant=variant))
     h = np.asarray(res.report.residual_history)
     target = ref_h[500]
     k = _iters_to_reach(h, target)
