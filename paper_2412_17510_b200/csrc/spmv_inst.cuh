@@ -81,7 +81,9 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
         sell_real_seg_kernel<K, MX><<<blocks, 128, 0, st>>>(S, xre, yre, ctx->seg_bounds, ctx->seg_T);
       else if (order == ORDER_FAST && MPSG_FUSED && K == 3 && A->xpad && td_pad_enabled()) {
         if constexpr (K == 3) {
-          pad_td_kernel<<<(unsigned)((A->ncols + 255) / 256), 256, 0, st>>>(xre, A->xpad, A->ncols);
+          // (host-call parts run in order on one stream: part 0 pads for all of them)
+          if (part <= 0)
+            pad_td_kernel<<<(unsigned)((A->ncols + 255) / 256), 256, 0, st>>>(xre, A->xpad, A->ncols);
           CUDA_TRY(ctx, launch_win(ctx, sell_real_kernel<K, ORDER_FAST, MX, true>, blocks, 128, 0, st, xre, xb, S,
                                    A->xpad, yre));
         }

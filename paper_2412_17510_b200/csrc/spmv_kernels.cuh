@@ -616,28 +616,28 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #ifndef MPSG_LONG_MX_U
 #define MPSG_LONG_MX_U 4
 #endif
-  if constexpr (!CPLX && MX && MPSG_LONG_MX_U > 1) {
-    // Mixed (8-byte values): U elements per lane per round, loads in flight
-    // together, accumulated in the lane's element order (same bits as U = 1)
-    constexpr int U = MPSG_LONG_MX_U;
+#ifndef MPSG_LONG_U_DD
+#define MPSG_LONG_U_DD 4
+#endif
+  if constexpr (!CPLX) {
+    // U elements per lane per round, accumulated in the lane's element order
+    // (the same bits for every U).  ptxas keeps the loads next to their uses
+    // whatever U is (40 registers for DD at U = 1..8, also with the loads in
+    // one asm block), so U only sets how often the level sums are swept.
+    constexpr int U = MX ? MPSG_LONG_MX_U : (K == 2 ? MPSG_LONG_U_DD : 2);
     for (; k + 32 * (U - 1) < e; k += 32 * U) {
       int c[U];
-      double a[U];
+      AVal<K, MX> a[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) c[u] = ld_s32_stream(L.col + k + 32 * u);
 #pragma unroll
-      for (int u = 0; u < U; ++u) a[u] = ld_f64_stream(L.val + k + 32 * u);
+      for (int u = 0; u < U; ++u) a[u].load(L.val, L.stride, k + 32 * u);
       MC<K> v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = load_aos<K>(xre, c[u]);
-      if constexpr (K >= 3) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) fma_lvl_d(acc[0], v[u], a[u]);
-        acc[0] = lvl_sweep(acc[0]);
-      } else {
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc[0] = fma_acc_d(acc[0], v[u], a[u]);
-      }
+      for (int u = 0; u < U; ++u) a[u].accumulate_lvl(acc[0], v[u]);
+      acc[0] = lvl_sweep(acc[0]);
     }
     for (; k < e; k += 32) {
       AVal<K, MX> a1;
@@ -645,17 +645,6 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
       a1.accumulate_lvl(acc[0], load_aos<K>(xre, ld_s32_stream(L.col + k)));
       acc[0] = lvl_sweep(acc[0]);
     }
-  } else if constexpr (!CPLX) {
-    int c = k < e ? ld_s32_stream(L.col + k) : 0;
-    for (int it = 0; k < e; k += 32, ++it) {
-      const int cn = k + 32 < e ? ld_s32_stream(L.col + k + 32) : 0;
-      AVal<K, MX> a;
-      a.load(L.val, L.stride, k);
-      a.accumulate_lvl(acc[0], load_aos<K>(xre, c));  // FAST: level sums, swept every four products
-      if ((it & 3) == 3) acc[0] = lvl_sweep(acc[0]);
-      c = cn;
-    }
-    acc[0] = lvl_sweep(acc[0]);
   } else {
     for (; k < e; k += 32) {
       const int c = ld_s32_stream(L.col + k);
