@@ -482,6 +482,10 @@ def run_gpu_spmv(args, cfg, K, order, rank, world, dist, variant="pure"):
                         "d2h_bytes_per_step": d2h, "call": e2e["call"], "host_memory": "pageable (numpy)"}
     if local_stats is not None:
         kernels = (1 if local_stats.nslices > 0 else 0) + (1 if local_stats.nlong > 0 else 0)
+        # real TD, FAST order, dense-enough matrices: x is first re-laid out to 32 bytes per element (pad_td_kernel)
+        if (K == 3 and not cplx and not mixed and order == 2 and nnz >= (1 << 20)
+                and nnz - local_stats.long_nnz >= 12 * local_stats.ncols):
+            kernels += 1
     else:
         kernels = 2  # upper bound for a shard (SELL + long-row kernel)
     # a working set that fits in L2 (config 1: 36 MB of 126 MB) also reported

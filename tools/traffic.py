@@ -28,7 +28,7 @@ SPECS.update({"cfg2_K4_mixed": "cfg2:4:2:mixed", "cfg4_K2_mixed": "cfg4:2:2:mixe
 
 def measure(spec):
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "-k", "regex:^(sell|long)_", "--csv",
+           "--clock-control", "none", "-k", "regex:^(sell|long|pad)_", "--csv",
            sys.executable, os.path.join(ROOT, "tools", "kbench.py"), "--steps", "1", "--warmup", "0", spec]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900).stdout
     rows = [r for r in csv.reader(io.StringIO(out[out.find('"ID"'):])) if r]
