@@ -1,7 +1,4 @@
 cd $GRAFT_REPO_ROOT
-S="cfg4:2:2"
-timeout 300 python tools/kbench.py --tag lu4 --steps 20 $S 2>&1 | grep -v "^#" | cut -c1-200
-for v in lu1 lu2 lu8; do
-MPSG_LIB=variants/$v.so timeout 300 python tools/kbench.py --tag $v --steps 20 $S 2>&1 | grep -v "^#" | cut -c1-200
-done
-timeout 600 python -m pytest tests/test_gpu_spmv.py tests/test_gpu_fast_accuracy.py -q -m gpu -x 2>&1 | tail -2
+S="cfg2:4:2 cfg5:4:2 cfg2:4:1 cfg2:4:0 cfg5:4:1"
+MPSG_LIB=variants/aos.so timeout 300 python tools/kbench.py --tag aos --steps 20 --check $S 2>&1 | grep -v "^#" | cut -c1-200
+timeout 300 python tools/kbench.py --tag base --steps 20 --check $S 2>&1 | grep -v "^#" | cut -c1-200
