@@ -12,7 +12,7 @@ import pytest
 import oracle as O
 import paper_2412_17510_b200 as M
 import synth
-from tests.util import bits_equal
+from tests.util import bits_equal, csr
 
 pytestmark = pytest.mark.gpu
 
@@ -202,6 +202,60 @@ def test_sharded_cg_several_ranks(P, K, variant):
     x = np.concatenate([p.x for p in parts])
     assert np.allclose(x[:, 0], xt[:, 0], atol=1e-12)
     assert parts[0].report.final_true_residual <= 10 * single.report.final_true_residual + 1e-30
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_one_reduction_cg_x0_breakdown_and_max_iterations(P):
+    """One-reduction sharded CG (the default over several ranks): an initial
+    guess (r0 = b - A x0 through the halo exchange), MaxIterations with an odd
+    iteration count and odd polling interval (both state parities), and the
+    reference's breakdown report -- every rank with the same report."""
+    K = 2
+    A = synth.config_matrix(5, K, 12)
+    xt = synth.config_vector(5, A.nrows, K)
+    b = O.spmv(A, xt, 1)
+    bounds = M.partition_rows(A.indptr, A.nrows, P)
+    x0 = (0.5 * xt[:, 0]).tolist()
+
+    def rank_fn(r, comm, ctx):
+        dA = M.DistCsr.from_global(comm, A, K, bounds=bounds)
+        lo, hi = dA.row_begin, dA.row_end
+        a = M.dsolve_cg(dA, b[lo:hi], M.SolverConfig(rel_tol=1e-22, max_iters=300, x0=x0, check_every=3))
+        m = M.dsolve_cg(dA, b[lo:hi], M.SolverConfig(rel_tol=1e-30, max_iters=7, check_every=3))
+        dA.close()
+        return a, m
+
+    parts = _run_ranks(P, rank_fn)
+    single = M.solve_cg(M.CsrOperator(M.DeviceCsr(A, K)), b, M.SolverConfig(rel_tol=1e-22, max_iters=300, x0=x0))
+    a0, m0 = parts[0]
+    for a, m in parts[1:]:
+        assert a.report.residual_history == a0.report.residual_history
+        assert m.report.residual_history == m0.report.residual_history
+    assert a0.report.status == single.report.status == M.SolverStatus.Converged
+    assert abs(a0.report.iterations - single.report.iterations) <= 1
+    assert abs(a0.report.residual_history[0] - single.report.residual_history[0]) <= 1e-12 * single.report.residual_history[0]
+    x = np.concatenate([p[0].x for p in parts])
+    assert np.allclose(x[:, 0], xt[:, 0], atol=1e-12)
+    assert m0.report.status == M.SolverStatus.MaxIterations and m0.report.iterations == 7
+    assert len(m0.report.residual_history) == 8
+
+    # skew-symmetric 2x2 blocks: <p, Ap> = 0 at the first step (test_krylov.cpp:193-211)
+    n = 8
+    S = csr(n, n, [[i ^ 1] for i in range(n)], 2,
+            planes=np.array([[1.0 if i % 2 == 0 else -1.0 for i in range(n)], [0.0] * n]))
+    sb = M.partition_rows(S.indptr, S.nrows, P)
+    ones = np.zeros((n, 2))
+    ones[:, 0] = 1.0
+
+    def rank_bd(r, comm, ctx):
+        dS = M.DistCsr.from_global(comm, S, 2, bounds=sb)
+        res = M.dsolve_cg(dS, ones[dS.row_begin:dS.row_end], M.SolverConfig())
+        dS.close()
+        return res.report
+
+    for rep in _run_ranks(P, rank_bd):
+        assert rep.status == M.SolverStatus.Breakdown and rep.iterations == 0
+        assert rep.detail == "cg: <p, Ap> vanished" and len(rep.residual_history) == 1
 
 
 # ---- row-sharded solve() for the other Krylov methods (mpsg_dsolve) ----------------
