@@ -78,6 +78,8 @@ enum DotPost {
 template <int K>
 MPSG_DI MC<K> block_reduce(MC<K> v, MC<K>* sh) {
   // fixed xor tree inside each warp, then warp partials in warp order
+  // (inlined and unrolled here: the called / looped tail that helps the
+  // solve() engine's larger reductions measured 1% slower for these kernels)
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = add(v, shfl_xor(v, off));
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;

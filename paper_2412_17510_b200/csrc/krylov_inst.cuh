@@ -229,7 +229,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         d[0] = KrTerm<K>{bi, bi};
       },
       [=] __device__(KrState<K> * s, MC<K> * d) {
-        const MC<K> bn = sqrt_mc(d[0]);
+        const MC<K> bn = sqrt_call(d[0]);
         s->thr = add(mul_d(bn, s->rel_tol), from_double<K>(s->abs_tol));
         s->rhs_norm = to_double(bn);
         s->cap = 1e6 * s->rhs_norm + 1e6 * s->abs_tol;
@@ -253,7 +253,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         d[0] = KrTerm<K>{ri, ri};
       },
       [=] __device__(KrState<K> * s, MC<K> * d) {
-        const MC<K> rn = sqrt_mc(d[0]);
+        const MC<K> rn = sqrt_call(d[0]);
         s->history[0] = to_double(rn);
         s->k = 0;
         s->status = less_equal(rn, s->thr) ? MPSG_CONVERGED : KR_RUNNING;
@@ -291,13 +291,13 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
     if (kr_tiny(to_double(d[0]), s->floor)) {
       kr_break(s, why);
     } else {
-      s->sc.alpha = divide(s->sc.rho, d[0]);
+      s->sc.alpha = divide_call(s->sc.rho, d[0]);
     }
   };
   // record_step on ||r|| = sqrt(d[0]); rho' = d[1]; beta = rho'/rho (BiCG, CGS)
   auto post_rho_next = [=] __device__(KrState<K> * s, MC<K> * d) {
     if (!kr_record(s, d[0])) return;
-    s->sc.beta = divide(d[1], s->sc.rho);
+    s->sc.beta = divide_call(d[1], s->sc.rho);
     s->sc.rho = d[1];
     kr_next(s, true);
   };
@@ -325,7 +325,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                  },
                  [=] __device__(KrState<K> * s, MC<K> * d) {
                    if (!kr_record(s, d[0])) return;
-                   s->sc.beta = divide(d[0], s->sc.rho);
+                   s->sc.beta = divide_call(d[0], s->sc.rho);
                    s->sc.rho = d[0];
                    kr_next(s, false);
                  })))
@@ -436,7 +436,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                      kr_break(s, 6);
                      return;
                    }
-                   const MC<K> om = divide(d[1], d[0]);
+                   const MC<K> om = divide_call(d[1], d[0]);
                    s->sc.omega = om;
                    if (kr_tiny(to_double(om), s->floor)) kr_break(s, 7);
                  })))
@@ -464,7 +464,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                    }
                    if (!kr_record(s, d[0])) return;
                    // beta = (rho'/rho) (alpha/omega) (:464-465)
-                   s->sc.beta = mul(divide(d[1], s->sc.rho), divide(s->sc.alpha, s->sc.omega));
+                   s->sc.beta = mul(divide_call(d[1], s->sc.rho), divide_call(s->sc.alpha, s->sc.omega));
                    s->sc.rho = d[1];
                    kr_next(s, true);
                  })))
@@ -519,7 +519,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                        kr_break(s, 8);
                        return;
                      }
-                     s->sc.zeta = divide(att, ata);
+                     s->sc.zeta = divide_call(att, ata);
                      s->sc.eta = zero<K>();
                    } else {
                      const MC<K> den = sub(mul(ata, yy), mul(yat, yat));
@@ -527,8 +527,8 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                        kr_break(s, 9);
                        return;
                      }
-                     s->sc.zeta = divide(sub(mul(yy, att), mul(yt, yat)), den);
-                     s->sc.eta = divide(sub(mul(ata, yt), mul(yat, att)), den);
+                     s->sc.zeta = divide_call(sub(mul(yy, att), mul(yt, yat)), den);
+                     s->sc.eta = divide_call(sub(mul(ata, yt), mul(yat, att)), den);
                    }
                  })))
           return e;
@@ -564,7 +564,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
                      kr_break(s, 10);
                      return;
                    }
-                   s->sc.beta = mul(divide(s->sc.alpha, s->sc.zeta), divide(d[1], s->sc.rho));
+                   s->sc.beta = mul(divide_call(s->sc.alpha, s->sc.zeta), divide_call(d[1], s->sc.rho));
                    s->sc.rho = d[1];
                    kr_next(s, true);
                  })))
@@ -640,7 +640,7 @@ int krylov_driver(mpsg_ctx* ctx, const mpsg_csr* A, const mpsg_dcsr* D, const mp
         const MC<K> wi = sub(load_aos_rw<K>(b, i), load_aos_rw<K>(q, i));
         d[0] = KrTerm<K>{wi, wi};
       },
-      [=] __device__(KrState<K> * s, MC<K> * d) { s->true_residual = to_double(sqrt_mc(d[0])); }));
+      [=] __device__(KrState<K> * s, MC<K> * d) { s->true_residual = to_double(sqrt_call(d[0])); }));
   double true_res = 0.0;
   KR_TRY(cudaMemcpyAsync(&true_res, &dst->true_residual, sizeof(double), cudaMemcpyDeviceToHost, st));
   const int64_t nh = iters + 1;

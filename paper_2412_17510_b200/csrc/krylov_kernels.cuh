@@ -108,7 +108,7 @@ MPSG_DI bool kr_record(KrState<K>* st, const MC<K>& d) {
   kr_pend(st, k, d);
   st->k = k;
   if (surely_continues(d, st->thr, st->cap)) return true;
-  const MC<K> rnorm = sqrt_mc(d);
+  const MC<K> rnorm = sqrt_call(d);
   const double rd = to_double(rnorm);
   st->history[k] = rd;
   if (!finite(rd)) {
@@ -131,7 +131,7 @@ MPSG_DI bool kr_record(KrState<K>* st, const MC<K>& d) {
 template <int K>
 MPSG_DI void kr_half_test(KrState<K>* st, const MC<K>& d) {
   if (surely_continues(d, st->thr, INFINITY)) return;
-  const MC<K> sn = sqrt_mc(d);
+  const MC<K> sn = sqrt_call(d);
   if (less_equal(sn, st->thr)) {
     st->k += 1;
     kr_pend(st, st->k, d);
@@ -172,8 +172,7 @@ MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh) {
   // fixed xor tree inside each warp, then warp partials in warp order
 #pragma unroll
   for (int m = 0; m < M; ++m) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) v[m] = add(v[m], shfl_xor(v[m], off));
+    v[m] = warp_tree(v[m]);
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {

@@ -945,4 +945,49 @@ MPSG_DI MC<K> shfl(const MC<K>& v, int src, unsigned mask = 0xffffffffu) {
   return r;
 }
 
+// The scalar tails of the solve() engine's reductions (krylov_kernels.cuh) run
+// once per launch on one thread, so their code is cold in the instruction
+// cache every time: for QD the multi-component divide / sqrt are called, not
+// inlined, and the warp tree is a loop (one copy of the add instead of five),
+// which keeps those kernels a fraction of their inlined size: cfg5 QD ms /
+// iteration BiCGSTAB 0.735 -> 0.685, GPBiCG 1.154 -> 1.070, CGS 0.596 -> 0.573
+// (MPSG_CG_SMALL_TAIL=0 restores the inlined form).
+#ifndef MPSG_CG_SMALL_TAIL
+#define MPSG_CG_SMALL_TAIL 1
+#endif
+template <int K>
+__device__ __noinline__ MC<K> divide_noinline(const MC<K>& a, const MC<K>& b) {
+  return divide(a, b);
+}
+template <int K>
+__device__ __noinline__ MC<K> sqrt_noinline(const MC<K>& a) {
+  return sqrt_mc(a);
+}
+// QD only: the DD / TD tails are short
+template <int K>
+MPSG_DI MC<K> divide_call(const MC<K>& a, const MC<K>& b) {
+  if constexpr (K == 4 && MPSG_CG_SMALL_TAIL)
+    return divide_noinline(a, b);
+  else
+    return divide(a, b);
+}
+template <int K>
+MPSG_DI MC<K> sqrt_call(const MC<K>& a) {
+  if constexpr (K == 4 && MPSG_CG_SMALL_TAIL)
+    return sqrt_noinline(a);
+  else
+    return sqrt_mc(a);
+}
+template <int K>
+MPSG_DI MC<K> warp_tree(MC<K> v) {
+  if constexpr (K == 4 && MPSG_CG_SMALL_TAIL) {
+#pragma unroll 1
+    for (int off = 16; off >= 1; off >>= 1) v = add(v, shfl_xor(v, off));
+  } else {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = add(v, shfl_xor(v, off));
+  }
+  return v;
+}
+
 }  // namespace mpsg
