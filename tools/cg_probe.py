@@ -15,6 +15,9 @@ xt = synth.config_vector(5, A.nrows, K)
 dA = M.DeviceCsr(A, K, ctx=ctx)
 b = M.spmv(dA, xt, M.ORDER_LANE4)
 cfg = M.SolverConfig(rel_tol=1e-30, max_iters=iters, fast=order == 2, lanes_enabled=order != 0)
-r = M.solve_cg(M.CsrOperator(dA), b, cfg)
-print(f"K={K} iters={r.report.iterations} device {r.report.device_seconds * 1e3 / iters:.3f} ms/iter "
+ts = []
+for _ in range(int(os.environ.get("CG_PROBE_REPS", "3"))):
+    r = M.solve_cg(M.CsrOperator(dA), b, cfg)
+    ts.append(r.report.device_seconds * 1e3 / iters)
+print(f"K={K} iters={r.report.iterations} device min {min(ts):.4f} median {sorted(ts)[len(ts) // 2]:.4f} ms/iter "
       f"wall {r.report.solve_seconds * 1e3 / iters:.3f} ms/iter")

@@ -1,5 +1,6 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2 3; do
-for lib in "" variants/before.so; do
-echo -n "lib=$lib  "; MPSG_LIB=$lib python tools/cg_probe.py 4 256
-done; done
+echo -n "base   "; python tools/cg_probe.py 4 256
+for v in dm3 dm4 t128m6 t128m8 t128; do
+echo -n "$v   "; MPSG_LIB=variants/$v.so python tools/cg_probe.py 4 256
+done
+echo -n "base   "; python tools/cg_probe.py 4 256
