@@ -990,4 +990,20 @@ MPSG_DI MC<K> warp_tree(MC<K> v) {
   return v;
 }
 
+// Load-grouping helpers (spmv_kernels.cuh, MPSG_TIE): w accumulates the xor
+// of one word of every loaded value; tie_apply xors it into a word of the
+// first operand TWICE (identity), through opaque asm so that neither NVVM nor
+// ptxas cancels it -- the first use of that operand then depends on every load.
+MPSG_DI uint32_t tie_word(uint32_t w, double v) {
+  uint32_t r;
+  asm("xor.b32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"((uint32_t)__double2loint(v)));
+  return r;
+}
+MPSG_DI double tie_apply(double v, uint32_t w) {
+  uint32_t lo = (uint32_t)__double2loint(v), t;
+  asm("xor.b32 %0, %1, %2;" : "=r"(t) : "r"(lo), "r"(w));
+  asm("xor.b32 %0, %1, %2;" : "=r"(lo) : "r"(t), "r"(w));
+  return __hiloint2double(__double2hiint(v), (int)lo);
+}
+
 }  // namespace mpsg

@@ -619,11 +619,17 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #ifndef MPSG_LONG_U_DD
 #define MPSG_LONG_U_DD 4
 #endif
+#ifndef MPSG_LONG_TIE
+#define MPSG_LONG_TIE 1
+#endif
   if constexpr (!CPLX) {
     // U elements per lane per round, accumulated in the lane's element order
-    // (the same bits for every U).  ptxas keeps the loads next to their uses
+    // (the same bits for every U).  ptxas keeps each load next to its use
     // whatever U is (40 registers for DD at U = 1..8, also with the loads in
-    // one asm block), so U only sets how often the level sums are swept.
+    // one asm block); for DD the first accumulate of a round is therefore made
+    // to depend on every load of the round (tie_word / tie_apply, an integer
+    // xor identity), which puts the round's 4 gathers and 8 value loads in
+    // flight together: cfg4 DD 587.8 -> 571.4 us.
     constexpr int U = MX ? MPSG_LONG_MX_U : (K == 2 ? MPSG_LONG_U_DD : 2);
     for (; k + 32 * (U - 1) < e; k += 32 * U) {
       int c[U];
@@ -635,6 +641,19 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
       MC<K> v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = load_aos<K>(xre, c[u]);
+#if MPSG_LONG_TIE
+      if constexpr (K == 2 && !MX) {
+        // every load of the round in flight before the first accumulate (tie_word)
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          w = tie_word(w, a[u].a.c[0]);
+          w = tie_word(w, a[u].a.c[1]);
+          w = tie_word(w, v[u].c[0]);
+        }
+        a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
+      }
+#endif
 #pragma unroll
       for (int u = 0; u < U; ++u) a[u].accumulate_lvl(acc[0], v[u]);
       acc[0] = lvl_sweep(acc[0]);
