@@ -25,6 +25,8 @@
 // componentwise bound).
 #pragma once
 
+#include <type_traits>
+
 #include "layout.h"
 #include "mc_arith.cuh"
 
@@ -116,6 +118,9 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 // accumulate (121 ops) the QD kernel is latency-limited: four products in
 // flight under a 64-register cap (MPSG_SELL_MINB 8) beat two (cfg2 QD 91.1 ->
 // 99.8 Gnnz/s); TD (52 ops) keeps two (G = 4 for TD: 126.3 -> 122.1).
+#ifndef MPSG_CPLX_TIE
+#define MPSG_CPLX_TIE 5
+#endif
 #ifndef MPSG_FUSED_G_QD
 #define MPSG_FUSED_G_QD 4
 #endif
@@ -443,6 +448,61 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
     }
     s1 = f1.finish();
     s2 = f2.finish();
+  } else if constexpr ((ORDER == ORDER_SCALAR || ORDER == ORDER_FAST) && K == 2 && !MX && MPSG_CPLX_TIE > 1) {
+    // DD (latency-bound): T elements per round, their column indices loaded a
+    // round ahead and their value pairs and four x gathers forced into flight
+    // together (tie_word, mc_arith.cuh); each sum still adds its terms in
+    // element order -- the same bits as one element per round.
+    constexpr int T = MPSG_CPLX_TIE;
+    int c[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) c[j] = j < len ? ld_s32_stream(cp + (int64_t)j * 16) : 0;
+    int k = 0;
+    // one round of T elements from k; PARTIAL: the row's last round, whose
+    // missing elements load the row's last one again (a valid address) and
+    // are not accumulated
+    auto round = [&](auto partial_tag) {
+      constexpr bool PARTIAL = decltype(partial_tag)::value;
+      int cn[T];
+#pragma unroll
+      for (int j = 0; j < T; ++j)
+        cn[j] = (!PARTIAL && k + T + j < len) ? ld_s32_stream(cp + (int64_t)(k + T + j) * 16) : 0;
+      AVal<K, MX> a[T];
+      MC<K> v1[T], v2[T];
+      const int last = PARTIAL ? len - 1 - k : T - 1;
+#pragma unroll
+      for (int j = 0; j < T; ++j) a[j].load(vp, st, (int64_t)(k + (PARTIAL ? min(j, last) : j)) * 16);
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        v1[j] = load_aos<K>(x1, c[j]);
+        v2[j] = load_aos<K>(x2, c[j]);
+      }
+      uint32_t w = 0;
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        w = tie_word(w, a[j].a.c[0]);
+        w = tie_word(w, a[j].a.c[1]);
+        w = tie_word(w, v1[j].c[0]);
+        w = tie_word(w, v2[j].c[0]);
+      }
+      a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        if (!PARTIAL || j <= last) {
+          if constexpr (ORDER == ORDER_FAST) {
+            s1 = a[j].accumulate(s1, v1[j]);
+            s2 = a[j].accumulate(s2, v2[j]);
+          } else {
+            s1 = add(s1, a[j].times(v1[j]));
+            s2 = add(s2, a[j].times(v2[j]));
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < T; ++j) c[j] = cn[j];
+    };
+    for (; k + T <= len; k += T) round(std::false_type{});
+    if (k < len) round(std::true_type{});
   } else if constexpr (ORDER == ORDER_SCALAR || ORDER == ORDER_FAST) {
     int c = len > 0 ? ld_s32_stream(cp) : 0;  // column index loaded a round ahead
     for (int k = 0; k < len; ++k) {
