@@ -702,16 +702,23 @@ __global__ void __launch_bounds__(128) long_fast_kernel(LongView L, const double
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = load_aos<K>(xre, c[u]);
 #if MPSG_LONG_TIE
-      if constexpr (K == 2 && !MX) {
+      if constexpr (K == 2) {
         // every load of the round in flight before the first accumulate (tie_word)
         uint32_t w = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          w = tie_word(w, a[u].a.c[0]);
-          w = tie_word(w, a[u].a.c[1]);
+          if constexpr (MX) {
+            w = tie_word(w, a[u].a);
+          } else {
+            w = tie_word(w, a[u].a.c[0]);
+            w = tie_word(w, a[u].a.c[1]);
+          }
           w = tie_word(w, v[u].c[0]);
         }
-        a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
+        if constexpr (MX)
+          a[0].a = tie_apply(a[0].a, w);
+        else
+          a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
       }
 #endif
 #pragma unroll
