@@ -118,6 +118,9 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 // accumulate (121 ops) the QD kernel is latency-limited: four products in
 // flight under a 64-register cap (MPSG_SELL_MINB 8) beat two (cfg2 QD 91.1 ->
 // 99.8 Gnnz/s); TD (52 ops) keeps two (G = 4 for TD: 126.3 -> 122.1).
+#ifndef MPSG_CPLX_TIE_L4
+#define MPSG_CPLX_TIE_L4 2
+#endif
 #ifndef MPSG_CPLX_TIE
 #define MPSG_CPLX_TIE 5
 #endif
@@ -537,7 +540,41 @@ __global__ void __launch_bounds__(128) sell_complex_kernel(SellView S, const dou
 #pragma unroll 1
     for (int j = 0; j < 4; ++j) {
       MC<K> L1 = zero<K>(), L2 = zero<K>();
-      for (int m = 0; m < nfull; ++m) {
+      int m = 0;
+      if constexpr (K == 2 && !MX && MPSG_CPLX_TIE_L4 > 1) {
+        // DD: T elements of the chain per round, loads tied into flight
+        // together (as the SCALAR / FAST branch above); same order, same bits
+        constexpr int T = MPSG_CPLX_TIE_L4;
+        for (; m + T <= nfull; m += T) {
+          int c[T];
+          AVal<K, MX> a[T];
+          MC<K> v1[T], v2[T];
+#pragma unroll
+          for (int t = 0; t < T; ++t) c[t] = ld_s32_stream(cp + (int64_t)(4 * (m + t) + j) * 16);
+#pragma unroll
+          for (int t = 0; t < T; ++t) a[t].load(vp, st, (int64_t)(4 * (m + t) + j) * 16);
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            v1[t] = load_aos<K>(x1, c[t]);
+            v2[t] = load_aos<K>(x2, c[t]);
+          }
+          uint32_t w = 0;
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            w = tie_word(w, a[t].a.c[0]);
+            w = tie_word(w, a[t].a.c[1]);
+            w = tie_word(w, v1[t].c[0]);
+            w = tie_word(w, v2[t].c[0]);
+          }
+          a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            L1 = add(L1, a[t].times(v1[t]));
+            L2 = add(L2, a[t].times(v2[t]));
+          }
+        }
+      }
+      for (; m < nfull; ++m) {
         const int64_t e = (int64_t)(4 * m + j) * 16;
         AVal<K, MX> a;
         a.load(vp, st, e);
