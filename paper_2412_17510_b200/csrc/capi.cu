@@ -476,6 +476,12 @@ int mpsg_csr_upload_ex(mpsg_ctx* ctx, int K, int flags, int64_t nrows, int64_t n
     else
       short_rows.push_back((int)i);
   }
+  // Long rows longest first: the exact orders run one serial chain (four with
+  // lanes on) per row, so the kernel ends when its longest row does -- a
+  // 50000-element row scheduled last would add its whole chain to the tail.
+  std::stable_sort(long_rows.begin(), long_rows.end(), [&](int a, int b) {
+    return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
+  });
   // Output parts for the host-pointer calls: consecutive sort windows write a
   // contiguous range of y rows (plus long rows, computed first), so the
   // device->host copy of part p overlaps the SELL launch of part p+1.

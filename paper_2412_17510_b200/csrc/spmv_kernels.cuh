@@ -653,10 +653,25 @@ __global__ void __launch_bounds__(128) long_det_kernel(LongView L, const double*
     if (chain) {
       if constexpr (SEG) {
         for (int i = 0; i < cnt; ++i) fold.push(L.col[b + c0 + i], prod[i * NS + sidx]);
-      } else if constexpr (ORDER == ORDER_LANE4) {
-        for (int i = lj; i < cnt && c0 + i < m4; i += 4) acc = add(acc, prod[i * NS + sidx]);
       } else {
-        for (int i = 0; i < cnt; ++i) acc = add(acc, prod[i * NS + sidx]);
+        // this chain's products: i = first, first + step, ... below lim; four
+        // shared-memory loads are tied into flight ahead of their four serial
+        // adds (tie_word, mc_arith.cuh) -- same order, same bits
+        constexpr int step = ORDER == ORDER_LANE4 ? 4 : 1;
+        const int lim = ORDER == ORDER_LANE4 ? (int)((m4 - c0) < cnt ? (m4 - c0) : cnt) : cnt;
+        int i = ORDER == ORDER_LANE4 ? lj : 0;
+        for (; i + 3 * step < lim; i += 4 * step) {
+          MC<K> q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) q[u] = prod[(i + u * step) * NS + sidx];
+          uint32_t w = 0;
+#pragma unroll
+          for (int u = 1; u < 4; ++u) w = tie_word(w, q[u].c[0]);
+          q[0].c[0] = tie_apply(q[0].c[0], w);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc = add(acc, q[u]);
+        }
+        for (; i < lim; i += step) acc = add(acc, prod[i * NS + sidx]);
       }
     }
     if (c0 + CH < len) __syncthreads();
