@@ -172,9 +172,9 @@ __global__ void MPSG_DOT_LB cg1r_dots_kernel(CgState<K>* S, int c, int init, int
     ag = pacc<F>(ag, rr, rr);
     ad = pacc<F>(ad, ww, rr);
   }
-  const MC<K> bg = block_reduce(ag, sh);
+  const MC<K> bg = block_reduce<K, F>(ag, sh);
   __syncthreads();
-  const MC<K> bd = block_reduce(ad, sh);
+  const MC<K> bd = block_reduce<K, F>(ad, sh);
   if (threadIdx.x == 0) {
     double* pp = partial + (int64_t)blockIdx.x * 2 * K;
 #pragma unroll
@@ -197,13 +197,18 @@ __global__ void MPSG_DOT_LB cg1r_dots_kernel(CgState<K>* S, int c, int init, int
       pg.c[j] = __ldcg(partial + (int64_t)b * 2 * K + j);
       pd.c[j] = __ldcg(partial + (int64_t)b * 2 * K + K + j);
     }
-    sg = add(sg, pg);
-    sd = add(sd, pd);
+    if constexpr (F && K >= 3 && MPSG_CG_LVL_TREE) {
+      lvl_add(sg, pg);
+      lvl_add(sd, pd);
+    } else {
+      sg = add(sg, pg);
+      sd = add(sd, pd);
+    }
   }
   __syncthreads();
-  const MC<K> tg = block_reduce(sg, sh);
+  const MC<K> tg = block_reduce<K, F>(sg, sh);
   __syncthreads();
-  const MC<K> td = block_reduce(sd, sh);
+  const MC<K> td = block_reduce<K, F>(sd, sh);
   if (threadIdx.x == 0) {
     S[0].ticket = 0u;
     if (local_out) {

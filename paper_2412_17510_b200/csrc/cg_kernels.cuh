@@ -30,6 +30,9 @@ constexpr int CG_RUNNING = -1;
 #else
 #define MPSG_DOT_LB __launch_bounds__(DOT_THREADS)
 #endif
+#ifndef MPSG_CG_LVL_TREE
+#define MPSG_CG_LVL_TREE 1
+#endif
 constexpr int DOT_THREADS = MPSG_DOT_THREADS;
 constexpr int DOT_MAX_BLOCKS = 1024;
 
@@ -75,13 +78,20 @@ enum DotPost {
   POST_TRUE = 4    // ||b - A x||: final true residual
 };
 
-template <int K>
+// F (FAST order, TD/QD): the tree combines on level sums (lvl_add), one sweep
+// and renormalisation at the end -- the tree is the serial tail of every
+// reduction kernel.
+template <int K, bool F = false>
 MPSG_DI MC<K> block_reduce(MC<K> v, MC<K>* sh) {
+  constexpr bool LV = F && K >= 3 && MPSG_CG_LVL_TREE;
   // fixed xor tree inside each warp, then warp partials in warp order
-  // (inlined and unrolled here: the called / looped tail that helps the
-  // solve() engine's larger reductions measured 1% slower for these kernels)
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) v = add(v, shfl_xor(v, off));
+  for (int off = 16; off >= 1; off >>= 1) {
+    if constexpr (LV)
+      lvl_add(v, shfl_xor(v, off));
+    else
+      v = add(v, shfl_xor(v, off));
+  }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) sh[w] = v;
   __syncthreads();
@@ -90,7 +100,13 @@ MPSG_DI MC<K> block_reduce(MC<K> v, MC<K>* sh) {
   if (w == 0) {
     const int nw = (int)(blockDim.x >> 5);
     if (lane < nw) s = sh[lane];
-    for (int off = nw >> 1; off >= 1; off >>= 1) s = add(s, shfl_xor(s, off));
+    for (int off = nw >> 1; off >= 1; off >>= 1) {
+      if constexpr (LV)
+        lvl_add(s, shfl_xor(s, off));
+      else
+        s = add(s, shfl_xor(s, off));
+    }
+    if constexpr (LV) s = canon(lvl_sweep(s));
   }
   return s;  // valid in thread 0
 }
@@ -164,11 +180,11 @@ MPSG_DI void cg_post(CgState<K>* st, int post, const MC<K>& d) {
 // tree) and runs the scalar step (or, multi-GPU, stores this rank's total in
 // local_out for the rank-ordered allgather sum).  Deterministic for a fixed
 // grid size.
-template <int K, int NT>
+template <int K, int NT, bool F = false>
 MPSG_DI void reduce_finish(CgState<K>* st, int post, MC<K> acc, double* partial, double* local_out, MC<K>* sh) {
   __shared__ bool last;
   const int G = gridDim.x;
-  MC<K> bsum = block_reduce(acc, sh);
+  MC<K> bsum = block_reduce<K, F>(acc, sh);
   if (threadIdx.x == 0) {
     double* pp = partial + (int64_t)blockIdx.x * K;
 #pragma unroll
@@ -185,10 +201,13 @@ MPSG_DI void reduce_finish(CgState<K>* st, int post, MC<K> acc, double* partial,
     MC<K> pv;
 #pragma unroll
     for (int j = 0; j < K; ++j) pv.c[j] = __ldcg(partial + (int64_t)i * K + j);
-    s = add(s, pv);
+    if constexpr (F && K >= 3 && MPSG_CG_LVL_TREE)
+      lvl_add(s, pv);
+    else
+      s = add(s, pv);
   }
   __syncthreads();
-  MC<K> tot = block_reduce(s, sh);
+  MC<K> tot = block_reduce<K, F>(s, sh);
   if (threadIdx.x == 0) {
     st->ticket = 0u;
     if (local_out) {
@@ -281,7 +300,7 @@ __global__ void MPSG_DOT_LB cg_reduce_kernel(CgState<K>* st, int post, int64_t n
   } else {
     for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) acc = add(acc, term(i));
   }
-  reduce_finish<K, DOT_THREADS>(st, post, acc, partial, local_out, sh);
+  reduce_finish<K, DOT_THREADS, F>(st, post, acc, partial, local_out, sh);
 }
 
 // Rank-ordered multi-component sum of the allgathered partials, then the

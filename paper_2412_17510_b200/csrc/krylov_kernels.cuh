@@ -167,12 +167,22 @@ MPSG_DI void kr_next(KrState<K>* st, bool check_rho) {
   }
 }
 
+// lv (FAST order with tree dots, TD/QD): the tree combines run on level sums
+// (lvl_add, mc_arith.cuh: QD 40 operations instead of the full add's 85) and
+// are swept / renormalised once at the end -- the trees are the serial tail of
+// every reduction kernel.
 template <int K, int M>
-MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh) {
+MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh, bool lv) {
   // fixed xor tree inside each warp, then warp partials in warp order
+  if (lv) {
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    v[m] = warp_tree(v[m]);
+    for (int m = 0; m < M; ++m) {
+#pragma unroll 1
+      for (int off = 16; off >= 1; off >>= 1) lvl_add(v[m], shfl_xor(v[m], off));
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = warp_tree(v[m]);
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
@@ -186,7 +196,12 @@ MPSG_DI void block_reduce_m(MC<K> (&v)[M], MC<K>* sh) {
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       MC<K> s = lane < nw ? sh[lane * M + m] : zero<K>();
-      for (int off = nw >> 1; off >= 1; off >>= 1) s = add(s, shfl_xor(s, off));
+      if (lv) {
+        for (int off = nw >> 1; off >= 1; off >>= 1) lvl_add(s, shfl_xor(s, off));
+        s = canon(lvl_sweep(s));
+      } else {
+        for (int off = nw >> 1; off >= 1; off >>= 1) s = add(s, shfl_xor(s, off));
+      }
       v[m] = s;
     }
   }
@@ -218,7 +233,8 @@ __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, i
 #pragma unroll
     for (int m = 0; m < M; ++m) acc[m] = sc.fused ? fma_acc(acc[m], t[m].a, t[m].b) : add(acc[m], mul(t[m].a, t[m].b));
   }
-  block_reduce_m<K, M>(acc, sh);
+  const bool lv = sc.fused && K >= 3;
+  block_reduce_m<K, M>(acc, sh, lv);
   if (threadIdx.x == 0) {
     double* pp = partial + (int64_t)blockIdx.x * M * K;
 #pragma unroll
@@ -241,10 +257,13 @@ __global__ void __launch_bounds__(KR_THREADS) kr_reduce_kernel(KrState<K>* st, i
       MC<K> pv;
 #pragma unroll
       for (int j = 0; j < K; ++j) pv.c[j] = __ldcg(partial + ((int64_t)b * M + m) * K + j);
-      s[m] = add(s[m], pv);
+      if (lv)
+        lvl_add(s[m], pv);
+      else
+        s[m] = add(s[m], pv);
     }
   }
-  block_reduce_m<K, M>(s, sh);
+  block_reduce_m<K, M>(s, sh, lv);
   if (threadIdx.x == 0) {
     st->ticket = 0u;
     if (local_out) {  // row-sharded: this rank's totals, summed across ranks by kr_post_gathered_kernel

@@ -616,6 +616,27 @@ MPSG_DI void fma_lvl_d(MC<3>& r, const MC<3>& x, double a) {
   r.c[2] = dfma(x.c[2], a, w);
 }
 MPSG_DI MC<2> lvl_sweep(const MC<2>& v) { return v; }
+// r += x on level sums (both operands may be unnormalised level sums): the
+// tree combines of the FAST-order reductions -- QD 40, TD 22 operations
+// instead of the full add's 85 / 83, swept and canonicalised once at the end.
+MPSG_DI void lvl_add(MC<4>& r, const MC<4>& x) {
+  double e0, f1, f2, g1, g2, g3;
+  two_sum(r.c[0], x.c[0], r.c[0], e0);
+  two_sum(r.c[1], x.c[1], r.c[1], f1);
+  two_sum(r.c[1], e0, r.c[1], f2);
+  two_sum(r.c[2], x.c[2], r.c[2], g1);
+  two_sum(r.c[2], f1, r.c[2], g2);
+  two_sum(r.c[2], f2, r.c[2], g3);
+  r.c[3] = dadd(dadd(dadd(dadd(r.c[3], x.c[3]), g1), g2), g3);
+}
+MPSG_DI void lvl_add(MC<3>& r, const MC<3>& x) {
+  double e0, f1, f2;
+  two_sum(r.c[0], x.c[0], r.c[0], e0);
+  two_sum(r.c[1], x.c[1], r.c[1], f1);
+  two_sum(r.c[1], e0, r.c[1], f2);
+  r.c[2] = dadd(dadd(dadd(r.c[2], x.c[2]), f1), f2);
+}
+MPSG_DI void lvl_add(MC<2>& r, const MC<2>& x) { r = add(r, x); }
 MPSG_DI MC<3> lvl_sweep(const MC<3>& v) {
   MC<3> r;
   double h;
