@@ -559,7 +559,7 @@ def run_gpu_cg(args, K, order, rank, world, dist, method="cg"):
     if dist:
         dist.barrier()
     loop, wall, res = [], [], None
-    for _ in range(max(1, args.steps // 5)):
+    for _ in range(max(3, args.steps // 5)):  # whole solves; medians below
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = solve()
