@@ -114,6 +114,38 @@ def test_edge_cases_empty_ragged_nonfinite(ctx, K):
         assert bits_equal(y, ref), first_mismatch(y, ref)
 
 
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_complex_ragged_rows_and_nonfinite(ctx, K):
+    """Complex rows of every length 0..13 and a few longer ones (the DD kernel
+    walks rounds of 5 elements, pairs in the LANE4 chains, with a partial last
+    round), NaN / Inf / signed zeros in x: both exact orders bit for bit, FAST
+    within the bound on the finite rows."""
+    rng = np.random.default_rng(40 + K)
+    n = 160
+    lens = list(range(14)) * 8 + [17, 21, 26, 33, 64, 65, 66, 70] * 6
+    rows = [sorted(rng.choice(n, size=L, replace=False).tolist()) for L in lens[:n]]
+    A = csr(n, n, rows, K, seed=21, is_complex=True)
+    xr = synth.vector(synth.VAL_NORMAL, n, K, seed=22)
+    xi = synth.vector(synth.VAL_NORMAL, n, K, seed=23)
+    dA = _upload(ctx, A, K, cplx=True)
+    yr, yi = M.spmv_complex(dA, xr, xi, M.ORDER_FAST)
+    rr, ri = O.spmv_complex(A, xr, xi, 0)
+    s = (O.abs_rowsum(A, A.planes[0], xr) + O.abs_rowsum(A, A.planes[K], xi) +
+         O.abs_rowsum(A, A.planes[0], xi) + O.abs_rowsum(A, A.planes[K], xr))
+    for y, ref in ((yr, rr), (yi, ri)):
+        ok, worst = bound_ok(A, xr, y, ref, K, extra=s)
+        assert ok and worst <= 0.25, worst
+    xr[3] = [np.inf] + [0.0] * (K - 1)
+    xi[5] = [np.nan] + [0.0] * (K - 1)
+    xr[7] = [-0.0] * K
+    xi[9] = [0.0] + [-0.0] * (K - 1)
+    for order in (0, 1):
+        yr, yi = M.spmv_complex(dA, xr, xi, order)
+        rr, ri = O.spmv_complex(A, xr, xi, order)
+        assert bits_equal(yr, rr), first_mismatch(yr, rr)
+        assert bits_equal(yi, ri), first_mismatch(yi, ri)
+
+
 def test_empty_and_zero_nnz_matrices(ctx):
     A = csr(0, 0, [], 2)
     y = M.spmv(_upload(ctx, A, 2), np.zeros((0, 2)), 1)
