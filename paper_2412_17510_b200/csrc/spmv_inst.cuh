@@ -47,13 +47,13 @@ int launch_spmv_mode(mpsg_ctx* ctx, const mpsg_csr* A, int order, const double* 
       const size_t smem = (size_t)CH * (CPLX ? 4 : 1) * sizeof(MC<K>);
       if (order == ORDER_SCALAR && ctx->seg_T > 1)
         long_det_kernel<K, ORDER_SCALAR, CPLX, CH, MX, CONJ, true>
-            <<<(int)A->nlong, 128, smem, lst>>>(L, xre, xim, yre, yim, ctx->seg_bounds, ctx->seg_T);
+            <<<(int)A->nlong, MPSG_LONG_DET_THREADS, smem, lst>>>(L, xre, xim, yre, yim, ctx->seg_bounds, ctx->seg_T);
       else if (order == ORDER_SCALAR)
         long_det_kernel<K, ORDER_SCALAR, CPLX, CH, MX, CONJ>
-            <<<(int)A->nlong, 128, smem, lst>>>(L, xre, xim, yre, yim);
+            <<<(int)A->nlong, MPSG_LONG_DET_THREADS, smem, lst>>>(L, xre, xim, yre, yim);
       else
         long_det_kernel<K, ORDER_LANE4, CPLX, CH, MX, CONJ>
-            <<<(int)A->nlong, 128, smem, lst>>>(L, xre, xim, yre, yim);
+            <<<(int)A->nlong, MPSG_LONG_DET_THREADS, smem, lst>>>(L, xre, xim, yre, yim);
     }
     CUDA_TRY(ctx, cudaGetLastError());
     if (fork) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));

@@ -624,8 +624,13 @@ MPSG_DI void long_products(const LongView& L, int64_t k, const double* __restric
   }
 }
 
+// Threads per CTA of the exact long-row kernel: the serial chains use 1 (SCALAR)
+// or 4 (LANE4) threads of a CTA, so smaller CTAs put more chains on an SM.
+#ifndef MPSG_LONG_DET_THREADS
+#define MPSG_LONG_DET_THREADS 128
+#endif
 template <int K, int ORDER, bool CPLX, int CH, bool MX, bool CONJ, bool SEG = false>
-__global__ void __launch_bounds__(128) long_det_kernel(LongView L, const double* __restrict__ xre,
+__global__ void __launch_bounds__(MPSG_LONG_DET_THREADS) long_det_kernel(LongView L, const double* __restrict__ xre,
                                                        const double* __restrict__ xim,
                                                        double* __restrict__ yre,
                                                        double* __restrict__ yim,
@@ -648,7 +653,39 @@ __global__ void __launch_bounds__(128) long_det_kernel(LongView L, const double*
   int64_t c0 = 0;
   for (; c0 < len; c0 += CH) {
     const int cnt = (int)((len - c0) < CH ? (len - c0) : CH);
-    for (int i = tid; i < cnt; i += blockDim.x) long_products<K, CPLX, MX>(L, b + c0 + i, xre, xim, prod + i * NS);
+    constexpr int NT = MPSG_LONG_DET_THREADS;
+    if constexpr (!CPLX && !MX && (CH % NT) == 0) {
+      // a full chunk: this thread's CH / NT elements with their columns,
+      // values and x gathers tied into flight together (tie_word,
+      // mc_arith.cuh); the products are the same bits
+      constexpr int E = CH / NT;
+      if (cnt == CH) {
+        int c[E];
+        AVal<K, MX> a[E];
+        MC<K> v[E];
+#pragma unroll
+        for (int u = 0; u < E; ++u) c[u] = L.col[b + c0 + tid + u * NT];
+#pragma unroll
+        for (int u = 0; u < E; ++u) a[u].load_ldg(L.val, L.stride, b + c0 + tid + u * NT);
+#pragma unroll
+        for (int u = 0; u < E; ++u) v[u] = load_aos<K>(xre, c[u]);
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+#pragma unroll
+          for (int q = 0; q < K; ++q) w = tie_word(w, a[u].a.c[q]);
+          w = tie_word(w, v[u].c[0]);
+          if constexpr (K > 2) w = tie_word(w, v[u].c[2]);
+        }
+        a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
+#pragma unroll
+        for (int u = 0; u < E; ++u) prod[(tid + u * NT) * NS] = a[u].times(v[u]);
+      } else {
+        for (int i = tid; i < cnt; i += blockDim.x) long_products<K, CPLX, MX>(L, b + c0 + i, xre, xim, prod + i * NS);
+      }
+    } else {
+      for (int i = tid; i < cnt; i += blockDim.x) long_products<K, CPLX, MX>(L, b + c0 + i, xre, xim, prod + i * NS);
+    }
     __syncthreads();
     if (chain) {
       if constexpr (SEG) {
