@@ -124,6 +124,9 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 #ifndef MPSG_CPLX_TIE
 #define MPSG_CPLX_TIE 5
 #endif
+#ifndef MPSG_DD_TAIL_TIE
+#define MPSG_DD_TAIL_TIE 1
+#endif
 #ifndef MPSG_FUSED_G_QD
 #define MPSG_FUSED_G_QD 4
 #endif
@@ -292,7 +295,42 @@ MPSG_DI MC<K> scalar_row(const double* __restrict__ vp, const int* __restrict__ 
 #pragma unroll
       for (int j = 0; j < G; ++j) acc = add(acc, p[j]);
     }
-    for (; k < len; ++k) acc = add(acc, sell_term<K, MX>(vp, cp, st, x, xw, k));
+#if MPSG_DD_TAIL_TIE
+    if constexpr (K == 2 && !MX) {
+      // the row's last 1..G-1 elements as one group: their columns, then their
+      // value pairs and x gathers, in flight together (tie_word, mc_arith.cuh;
+      // slots past the row's end repeat its last element and are not added)
+      // instead of one element -- two dependent round trips -- at a time
+      const int rem = len - k;
+      if (rem == 1) {
+        acc = add(acc, sell_term<K, MX>(vp, cp, st, x, xw, k));
+      } else if (rem > 1) {
+        int c[G - 1];
+        AVal<K, MX> a[G - 1];
+        MC<K> v[G - 1];
+#pragma unroll
+        for (int j = 0; j < G - 1; ++j) c[j] = ld_s32_stream(cp + (int64_t)(k + min(j, rem - 1)) * 32);
+#pragma unroll
+        for (int j = 0; j < G - 1; ++j) a[j].load(vp, st, (int64_t)(k + min(j, rem - 1)) * 32);
+#pragma unroll
+        for (int j = 0; j < G - 1; ++j) v[j] = load_x<K>(x, xw, c[j]);
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < G - 1; ++j) {
+          w = tie_word(w, a[j].a.c[0]);
+          w = tie_word(w, a[j].a.c[1]);
+          w = tie_word(w, v[j].c[0]);
+        }
+        a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
+#pragma unroll
+        for (int j = 0; j < G - 1; ++j)
+          if (j < rem) acc = add(acc, a[j].times(v[j]));
+      }
+    } else
+#endif
+    {
+      for (; k < len; ++k) acc = add(acc, sell_term<K, MX>(vp, cp, st, x, xw, k));
+    }
     return acc;
   }
 }
