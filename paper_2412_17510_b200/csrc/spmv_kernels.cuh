@@ -127,6 +127,12 @@ struct AVal<K, true> {  // Mixed: one binary64 plane, mul_by_double(v, a)
 #ifndef MPSG_DD_TAIL_TIE
 #define MPSG_DD_TAIL_TIE 1
 #endif
+#ifndef MPSG_DD_L4_MINB
+#define MPSG_DD_L4_MINB 10
+#endif
+#ifndef MPSG_DD_L4_TAIL_TIE
+#define MPSG_DD_L4_TAIL_TIE 1
+#endif
 #ifndef MPSG_FUSED_G_QD
 #define MPSG_FUSED_G_QD 4
 #endif
@@ -211,6 +217,37 @@ MPSG_DI MC<K> lane4_row(const double* __restrict__ vp, const int* __restrict__ c
 #pragma unroll
     for (int c = 0; c < P; ++c) s = add(s, L[c]);
   }
+#if MPSG_DD_L4_TAIL_TIE
+  if constexpr (K == 2 && !MX) {
+    // the remainder (1-3 elements) as one tied group, as in scalar_row
+    const int k0 = nfull * 4, rem = len - k0;
+    if (rem == 1) {
+      s = add(s, sell_term<K, MX>(vp, cp, st, x, xw, k0));
+    } else if (rem > 1) {
+      int c[3];
+      AVal<K, MX> a[3];
+      MC<K> v[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) c[j] = ld_s32_stream(cp + (int64_t)(k0 + min(j, rem - 1)) * 32);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) a[j].load(vp, st, (int64_t)(k0 + min(j, rem - 1)) * 32);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) v[j] = load_x<K>(x, xw, c[j]);
+      uint32_t w = 0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        w = tie_word(w, a[j].a.c[0]);
+        w = tie_word(w, a[j].a.c[1]);
+        w = tie_word(w, v[j].c[0]);
+      }
+      a[0].a.c[0] = tie_apply(a[0].a.c[0], w);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (j < rem) s = add(s, a[j].times(v[j]));
+    }
+    return s;
+  }
+#endif
   for (int k = nfull * 4; k < len; ++k) s = add(s, sell_term<K, MX>(vp, cp, st, x, xw, k));
   return s;
 }
@@ -405,10 +442,11 @@ template <int K, int ORDER, bool MX, bool XW>
 __global__ void MPSG_SELL_LB sell_real_kernel(SellView S, const double* __restrict__ x, double* __restrict__ y) {
   sell_real_body<K, ORDER, MX, XW>(S, x, y);
 }
-// DD in the LANE4 order is memory-latency-bound: capped at 40 registers for
-// 12 resident blocks per SM (measured +17% on config 5, profiles/r01b_*).
+// DD in the LANE4 order is memory-latency-bound: a resident-block floor (12
+// blocks / 40 registers measured +17% on config 5 in round 1; 10 blocks / 48
+// registers with the tied remainder group, round 2: cfg5 DD LANE4 71.7 -> 67.6 us).
 template <int K, bool MX>
-__global__ void __launch_bounds__(128, 12) sell_real_lane4_lat_kernel(SellView S, const double* __restrict__ x,
+__global__ void __launch_bounds__(128, MPSG_DD_L4_MINB) sell_real_lane4_lat_kernel(SellView S, const double* __restrict__ x,
                                                                      double* __restrict__ y) {
   sell_real_body<K, ORDER_LANE4, MX, false>(S, x, y);
 }
