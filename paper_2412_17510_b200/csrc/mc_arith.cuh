@@ -870,8 +870,23 @@ MPSG_DI int ld_s32_stream(const int* q) {
 #endif
 }
 
+// 256-bit x gathers: 0 ld.global.nc (L1-allocating), 1 ld.global.cg, 2 nc with
+// L1::no_allocate, 3 nc with L1::evict_last.  Random gathers find almost nothing
+// in L1 (1% hit rate in ncu), so not allocating is the default: cfg2 TD 195.6 ->
+// 189.5 us (three alternating runs), QD and cfg5 unchanged.
+#ifndef MPSG_X_LD
+#define MPSG_X_LD 2
+#endif
 MPSG_DI void ld_v4(const double* q, double& a, double& b, double& c, double& d) {
+#if MPSG_X_LD == 1
+  asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(q));
+#elif MPSG_X_LD == 2
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(q));
+#elif MPSG_X_LD == 3
+  asm("ld.global.nc.L1::evict_last.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(q));
+#else
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(q));
+#endif
 }
 // QD gather of x[i] as one 256-bit load (LDG.E.ENL2.256, sm_100; the caller
 // guarantees p is 32-byte aligned) instead of two 128-bit ones: one L1
