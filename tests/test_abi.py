@@ -118,3 +118,28 @@ def test_null_arguments_rejected():
     assert L.mpsg_cg(None, None, 0, 0, None, None, None, None, None, 0, None) == M.E_ARG
     assert L.mpsg_partition_rows(None, 0, 1, None) == M.E_ARG
     assert L.mpsg_last_error(None) == b"null context"
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of the ABI structs have the sizes the C compiler gives
+    the declarations in include/mpsg.h (a field added on one side only would
+    silently shift everything after it)."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "sizes.c"
+    src.write_text('#include <stdio.h>\n#include "mpsg.h"\n'
+                   'int main(void) { printf("%zu %zu %zu %zu\\n", sizeof(mpsg_cg_config), '
+                   'sizeof(mpsg_solver_config), sizeof(mpsg_cg_report), sizeof(mpsg_csr_stats)); return 0; }\n')
+    exe = tmp_path / "sizes"
+    subprocess.run(["gcc", "-I", os.path.join(root, "include"), "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert [int(v) for v in out] == [ctypes.sizeof(M._CgConfig), ctypes.sizeof(M._SolverConfig),
+                                     ctypes.sizeof(M._CgReport), ctypes.sizeof(M.CsrStats)]
+
+
+def test_solver_config_validates_the_cg_variant():
+    for v in (0, 1, 2):
+        M.SolverConfig(cg_variant=v).validate()
+    with pytest.raises(ValueError, match="cg_variant"):
+        M.SolverConfig(cg_variant=3).validate()
